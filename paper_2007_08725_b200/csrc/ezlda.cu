@@ -1,0 +1,990 @@
+// ezlda.cu -- C ABI (include/ezlda.h) and host orchestration of the ezLDA hot path.
+//
+// create:  inputs -> device; doc-major order (doc, word, input position) by a CUB radix
+//          sort; words relabelled by count; (doc, word) runs; word-major run
+//          order (the word-sorted token list T of P:845, at run granularity); the
+//          sampler's work list with large-word dissection; z^0 from
+//          Philox; W^0 / n_k^0.  All on the device except O(V) / O(items) host sorts.
+// iterate: den + word-prep -> doc pass -> sampler (+ W all-reduce when world > 1),
+//          one stream, no host round trip.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/ezlda.h"
+#include "kernels.h"
+
+using ezl::Buf;
+using ezl::Dev;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// ----------------------------------------------------------------------------
+// NCCL, loaded at run time (only when world > 1).
+// ----------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+// ----------------------------------------------------------------------------
+// setup kernels
+// ----------------------------------------------------------------------------
+__global__ void k_max_u32(const uint32_t* a, uint64_t n, uint32_t* out) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, a[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_hist(const uint32_t* a, uint64_t n, uint32_t* h) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[a[i]], 1u);
+}
+
+__global__ void k_make_keys(const uint32_t* word, const uint32_t* doc, uint32_t n, uint64_t* key, uint32_t* idx) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    key[i] = ((uint64_t)doc[i] << 32) | word[i];
+    idx[i] = i;
+  }
+}
+
+// tw[j] = newword[word(j)]; head[j] = 1 iff a (doc, word) run starts at j
+__global__ void k_tw_heads(const uint64_t* key, uint32_t n, const uint32_t* newword, uint32_t* tw, uint32_t* head) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const uint64_t k = key[j];
+    tw[j] = newword[(uint32_t)k];
+    head[j] = (j == 0 || key[j - 1] != k) ? 1u : 0u;
+  }
+}
+
+// per doc-major run q (qidx = inclusive scan of heads - 1)
+__global__ void k_run_heads(const uint64_t* key, const uint32_t* head, const uint32_t* qinc, const uint32_t* tw,
+                            uint32_t n, uint32_t* q_j0, uint32_t* q_v, uint32_t* q_doc) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n && head[j]) {
+    const uint32_t q = qinc[j] - 1;
+    q_j0[q] = j;
+    q_v[q] = tw[j];
+    q_doc[q] = (uint32_t)(key[j] >> 32);
+  }
+}
+
+__global__ void k_iota(uint32_t* a, uint32_t n) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+// word-major run tables from the sorted run permutation
+__global__ void k_run_tables(const uint32_t* rperm, uint32_t R, uint32_t N, const uint32_t* q_j0, const uint32_t* q_doc,
+                             const uint32_t* dofs, uint32_t* run_j0, uint32_t* run_dbase, uint16_t* run_len,
+                             uint32_t* len32, uint32_t* rid_of_q) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) {
+    const uint32_t q = rperm[r];
+    const uint32_t j0 = q_j0[q];
+    const uint32_t j1 = (q + 1 < R) ? q_j0[q + 1] : N;
+    const uint32_t d = q_doc[q];
+    run_j0[r] = j0;
+    run_dbase[r] = dofs[d] + 2u * d;
+    run_len[r] = (uint16_t)(j1 - j0);
+    len32[r] = j1 - j0;
+    rid_of_q[q] = r;
+  }
+}
+
+__global__ void k_trid(const uint32_t* qinc, const uint32_t* rid_of_q, uint32_t n, uint32_t* trid) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) trid[j] = rid_of_q[qinc[j] - 1];
+}
+
+// wrun[v] = first run of word v (lower bound in the sorted run words), v in [0, V]
+__global__ void k_wrun(const uint32_t* vs, uint32_t R, uint32_t V, uint32_t* wrun) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v <= V) {
+    uint32_t lo = 0, hi = R;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (vs[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    wrun[v] = lo;
+  }
+}
+
+// item heads: first run of each word, and dense-word region boundaries every `split` tokens
+__global__ void k_item_heads(const uint32_t* vs, const uint32_t* wrun, const uint32_t* tokpre, uint32_t R, uint32_t Vd,
+                             uint32_t split, uint32_t* head) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) {
+    const uint32_t v = vs[r];
+    const uint32_t first = wrun[v];
+    uint32_t h = (r == first);
+    if (!h && v < Vd) {
+      const uint32_t b = tokpre[first];
+      h = ((tokpre[r] - b) / split) != ((tokpre[r - 1] - b) / split);
+    }
+    head[r] = h;
+  }
+}
+
+__global__ void k_items(const uint32_t* r0s, uint32_t NI, uint32_t R, const uint32_t* vs, const uint32_t* tokpre,
+                        uint32_t* item4) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < NI) {
+    const uint32_t r0 = r0s[i];
+    const uint32_t r1 = (i + 1 < NI) ? r0s[i + 1] : R;
+    item4[4 * i + 0] = vs[r0];
+    item4[4 * i + 1] = r0;
+    item4[4 * i + 2] = r1;
+    item4[4 * i + 3] = tokpre[r1] - tokpre[r0];
+  }
+}
+
+inline unsigned blocks(uint64_t n, unsigned t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// the handle
+// ----------------------------------------------------------------------------
+struct ezlda {
+  Dev dev{};
+  Buf buf[2]{};
+  int cur = 0;
+  std::vector<void*> allocs;  // device allocations owned by the handle
+  uint64_t N = 0;
+  uint32_t Dn = 0, V = 0, K = 0, R = 0, Vd = 0, Vt = 0;
+  uint32_t n_items = 0, n_docs_w = 0, n_docs_b = 0;
+  uint64_t tail_cap = 0;
+  double alpha = 0, beta = 0;
+  uint64_t seed = 0;
+  uint32_t g = 2;
+  int rank = 0, world = 1;
+  uint64_t N_global = 0;
+  uint32_t* docs_w = nullptr;
+  uint32_t* docs_b = nullptr;
+  uint32_t* perm = nullptr;
+  std::vector<uint32_t> newword, origword;  // orig -> relabelled, relabelled -> orig
+  uint32_t iteration = 0;
+  bool D_fresh = false;  // D rows describe buf[cur].z
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool timing = true;
+  // per-iteration records (events + pinned counter copies), folded lazily into stats
+  static constexpr int kSlots = 256;
+  struct Slot {
+    cudaEvent_t ev[5];
+    uint32_t iteration;
+    uint32_t launches;
+  };
+  std::vector<Slot> slots;
+  std::vector<int> pending;  // FIFO of slot indices not yet folded
+  uint64_t slot_counter = 0;
+  ezl::Counters* ctr_host = nullptr;  // pinned, kSlots entries
+  ezlda_iter_stats sum{};
+  uint32_t sum_n = 0;
+  double* llpt_partial = nullptr;
+  double* llpt_out = nullptr;
+  ncclComm_t comm = nullptr;
+  ezlda_status sticky = EZLDA_OK;
+  std::string err;
+  ezlda_iter_stats last{};
+
+  ezlda_status fail(ezlda_status s, const char* fmt, ...) {
+    char b[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof b, fmt, ap);
+    va_end(ap);
+    err = b;
+    if (s == EZLDA_E_CUDA || s == EZLDA_E_NCCL) sticky = s;
+    return s;
+  }
+
+  template <typename T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  void release(void* p) {
+    auto it = std::find(allocs.begin(), allocs.end(), p);
+    if (it != allocs.end()) {
+      cudaFree(p);
+      allocs.erase(it);
+    }
+  }
+};
+
+#define EZ_CUDA(h, call)                                                                                   \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess) return (h)->fail(EZLDA_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,       \
+                                            cudaGetErrorString(e_));                                       \
+  } while (0)
+#define EZ_ALLOC(h, ptr, T, n)                                                                             \
+  do {                                                                                                     \
+    (ptr) = (h)->alloc<T>(n);                                                                              \
+    if (!(ptr)) return (h)->fail(EZLDA_E_NOMEM, "cudaMalloc of %zu x %zu bytes failed (%s)", (size_t)(n),  \
+                                 sizeof(T), #ptr);                                                         \
+  } while (0)
+#define EZ_NCCL(h, call)                                                                                   \
+  do {                                                                                                     \
+    ncclResult_t r_ = (call);                                                                              \
+    if (r_ != ncclSuccess) return (h)->fail(EZLDA_E_NCCL, "%s: %s", #call, nccl().GetErrorString(r_));     \
+  } while (0)
+
+namespace {
+
+// CUB wrappers (setup only)
+template <typename F>
+ezlda_status cub_call(ezlda* h, F f) {
+  size_t bytes = 0;
+  if (f(nullptr, bytes) != cudaSuccess) return h->fail(EZLDA_E_CUDA, "cub size query failed");
+  void* tmp = nullptr;
+  if (cudaMalloc(&tmp, std::max<size_t>(bytes, 1)) != cudaSuccess) return h->fail(EZLDA_E_NOMEM, "cub temp alloc");
+  cudaError_t e = f(tmp, bytes);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return h->fail(EZLDA_E_CUDA, "cub call failed: %s", cudaGetErrorString(e));
+  return EZLDA_OK;
+}
+
+ezlda_status allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
+  if (h->world <= 1 || count == 0) return EZLDA_OK;
+  EZ_NCCL(h, nccl().AllReduce(buf, buf, count, dt, ncclSum, h->comm, h->stream));
+  return EZLDA_OK;
+}
+
+void fill_dev(ezlda* h) {
+  Dev& d = h->dev;
+  d.N = (uint32_t)h->N;
+  d.Dn = h->Dn;
+  d.V = h->V;
+  d.K = h->K;
+  d.nch = (h->K + 31) / 32;
+  d.Kpad = d.nch * 32;
+  d.Vd = h->Vd;
+  d.geff = std::min<uint32_t>(h->g, h->K - 1);
+  d.alpha = h->alpha;
+  d.beta = h->beta;
+  d.Vbeta = (double)h->V * h->beta;
+  d.seed = h->seed;
+}
+
+// W^cur and n_k^cur from buf[cur].z (init / set_topics), + all-reduce
+ezlda_status rebuild_counts(ezlda* h) {
+  Buf& b = h->buf[h->cur];
+  EZ_CUDA(h, cudaMemsetAsync(b.Wd, 0, sizeof(int32_t) * (size_t)h->Vd * h->K, h->stream));
+  EZ_CUDA(h, cudaMemsetAsync(b.nk, 0, sizeof(int32_t) * h->K, h->stream));
+  EZ_CUDA(h, cudaMemsetAsync(b.tnnz, 0, sizeof(uint32_t) * std::max<uint32_t>(h->Vt, 1), h->stream));
+  ezl::launch_sampler(h->dev, b, b, h->n_items, 0, true, h->stream);
+  EZ_CUDA(h, cudaGetLastError());
+  ezlda_status s;
+  if ((s = allreduce(h, b.Wd, (size_t)h->Vd * h->K, ncclInt32))) return s;
+  if ((s = allreduce(h, b.nk, h->K, ncclInt32))) return s;
+  h->D_fresh = false;
+  return EZLDA_OK;
+}
+
+ezlda_status ensure_D(ezlda* h) {
+  if (h->D_fresh) return EZLDA_OK;
+  Buf& b = h->buf[h->cur];
+  ezl::launch_doc_pass(h->dev, b, b, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, h->iteration, false, h->stream);
+  EZ_CUDA(h, cudaGetLastError());
+  h->D_fresh = true;
+  return EZLDA_OK;
+}
+
+ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_ids, const ezlda_options& o) {
+  const uint32_t N = (uint32_t)h->N;
+  cudaStream_t s = h->stream;
+  // ---- inputs on device
+  uint32_t *d_word, *d_doc;
+  EZ_ALLOC(h, d_word, uint32_t, N);
+  EZ_ALLOC(h, d_doc, uint32_t, N);
+  const cudaMemcpyKind kind = o.input_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  EZ_CUDA(h, cudaMemcpyAsync(d_word, word_ids, sizeof(uint32_t) * N, kind, s));
+  EZ_CUDA(h, cudaMemcpyAsync(d_doc, doc_ids, sizeof(uint32_t) * N, kind, s));
+  // ---- validate ids
+  uint32_t* d_max;
+  EZ_ALLOC(h, d_max, uint32_t, 2);
+  EZ_CUDA(h, cudaMemsetAsync(d_max, 0, 8, s));
+  k_max_u32<<<1184, 256, 0, s>>>(d_word, N, d_max);
+  k_max_u32<<<1184, 256, 0, s>>>(d_doc, N, d_max + 1);
+  uint32_t mx[2];
+  EZ_CUDA(h, cudaMemcpyAsync(mx, d_max, 8, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  if (mx[0] >= h->V) return h->fail(EZLDA_E_INVALID, "word id %u >= V = %u", mx[0], h->V);
+  if (mx[1] >= h->Dn) return h->fail(EZLDA_E_INVALID, "doc id %u >= n_docs = %u", mx[1], h->Dn);
+  // ---- doc lengths, word counts
+  uint32_t *d_L, *d_cnt;
+  EZ_ALLOC(h, d_L, uint32_t, h->Dn);
+  EZ_ALLOC(h, d_cnt, uint32_t, h->V);
+  EZ_CUDA(h, cudaMemsetAsync(d_L, 0, sizeof(uint32_t) * h->Dn, s));
+  EZ_CUDA(h, cudaMemsetAsync(d_cnt, 0, sizeof(uint32_t) * h->V, s));
+  k_hist<<<2368, 256, 0, s>>>(d_doc, N, d_L);
+  k_hist<<<2368, 256, 0, s>>>(d_word, N, d_cnt);
+  std::vector<uint32_t> L(h->Dn), cnt_local(h->V);
+  EZ_CUDA(h, cudaMemcpyAsync(L.data(), d_L, sizeof(uint32_t) * h->Dn, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaMemcpyAsync(cnt_local.data(), d_cnt, sizeof(uint32_t) * h->V, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  for (uint32_t d = 0; d < h->Dn; ++d)
+    if (L[d] > 65535) return h->fail(EZLDA_E_RANGE, "doc %u has %u tokens (> 65535, P:753)", d, L[d]);
+  std::vector<uint32_t> dofs(h->Dn + 1, 0);
+  for (uint32_t d = 0; d < h->Dn; ++d) dofs[d + 1] = dofs[d] + L[d];
+  if ((uint64_t)N + 2ull * h->Dn >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "tokens + 2 docs >= 2^32 per shard");
+  // global word counts (the dense/tail split and relabelling must agree on all ranks)
+  std::vector<uint64_t> cnt(h->V);
+  for (uint32_t v = 0; v < h->V; ++v) cnt[v] = cnt_local[v];
+  if (h->world > 1) {
+    uint64_t* d_c64;
+    EZ_ALLOC(h, d_c64, uint64_t, h->V);
+    EZ_CUDA(h, cudaMemcpyAsync(d_c64, cnt.data(), sizeof(uint64_t) * h->V, cudaMemcpyHostToDevice, s));
+    ezlda_status st = allreduce(h, d_c64, h->V, ncclUint64);
+    if (st) return st;
+    EZ_CUDA(h, cudaMemcpyAsync(cnt.data(), d_c64, sizeof(uint64_t) * h->V, cudaMemcpyDeviceToHost, s));
+    uint64_t nl = N, ng = 0;
+    uint64_t* d_n;
+    EZ_ALLOC(h, d_n, uint64_t, 1);
+    EZ_CUDA(h, cudaMemcpyAsync(d_n, &nl, 8, cudaMemcpyHostToDevice, s));
+    if ((st = allreduce(h, d_n, 1, ncclUint64))) return st;
+    EZ_CUDA(h, cudaMemcpyAsync(&ng, d_n, 8, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    h->N_global = ng;
+    h->release(d_c64);
+    h->release(d_n);
+  } else {
+    h->N_global = N;
+  }
+  // ---- relabel words by count desc, ties by id
+  h->origword.resize(h->V);
+  std::iota(h->origword.begin(), h->origword.end(), 0u);
+  std::stable_sort(h->origword.begin(), h->origword.end(),
+                   [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
+  h->newword.resize(h->V);
+  for (uint32_t i = 0; i < h->V; ++i) h->newword[h->origword[i]] = i;
+  // dense iff c_v > threshold ("larger than the topic number"); counts > 65535 must be dense
+  // (words are sorted by count, so the dense set is a prefix of the relabelled ids)
+  uint64_t thr = o.dense_threshold ? o.dense_threshold : h->K;
+  if (o.w_mode == EZLDA_W_ALL_SPARSE) thr = 65535;  // tail counts must fit 16 bits
+  uint32_t Vd = 0;
+  while (Vd < h->V && (cnt[h->origword[Vd]] > thr || cnt[h->origword[Vd]] > 65535)) ++Vd;
+  // world > 1: W is merged by an int32 all-reduce of dense rows (tail all-gather: next round)
+  if (o.w_mode == EZLDA_W_ALL_DENSE || h->world > 1) Vd = h->V;
+  h->Vd = Vd;
+  h->Vt = h->V - Vd;
+  std::vector<uint32_t> tofs(h->Vt + 1, 0);
+  for (uint32_t t = 0; t < h->Vt; ++t)
+    tofs[t + 1] = tofs[t] + (uint32_t)std::min<uint64_t>(cnt[h->origword[Vd + t]], h->K);
+  h->tail_cap = tofs[h->Vt];
+  std::vector<uint32_t> wtok(h->V + 1, 0);
+  for (uint32_t v = 0; v < h->V; ++v) wtok[v + 1] = wtok[v] + cnt_local[h->origword[v]];
+  // ---- doc-major order: sort (doc, word, input position)
+  uint64_t *k_in, *k_out;
+  uint32_t *i_in, *i_out;
+  EZ_ALLOC(h, k_in, uint64_t, N);
+  EZ_ALLOC(h, k_out, uint64_t, N);
+  EZ_ALLOC(h, i_in, uint32_t, N);
+  EZ_ALLOC(h, i_out, uint32_t, N);
+  k_make_keys<<<blocks(N), 256, 0, s>>>(d_word, d_doc, N, k_in, i_in);
+  int dbits = 1;
+  while (dbits < 32 && ((h->Dn - 1) >> dbits)) ++dbits;
+  ezlda_status st;
+  st = cub_call(h, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, k_in, k_out, i_in, i_out, (int)N, 0, 32 + dbits, s);
+  });
+  if (st) return st;
+  h->release(k_in);
+  h->release(i_in);
+  h->release(d_word);
+  h->release(d_doc);
+  h->perm = i_out;
+  // ---- relabelled word per token, run heads
+  uint32_t *d_newword, *tw, *head, *qinc;
+  EZ_ALLOC(h, d_newword, uint32_t, h->V);
+  EZ_CUDA(h, cudaMemcpyAsync(d_newword, h->newword.data(), sizeof(uint32_t) * h->V, cudaMemcpyHostToDevice, s));
+  EZ_ALLOC(h, tw, uint32_t, N);
+  EZ_ALLOC(h, head, uint32_t, N);
+  EZ_ALLOC(h, qinc, uint32_t, N);
+  k_tw_heads<<<blocks(N), 256, 0, s>>>(k_out, N, d_newword, tw, head);
+  st = cub_call(h, [&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, head, qinc, (int)N, s); });
+  if (st) return st;
+  uint32_t R = 0;
+  EZ_CUDA(h, cudaMemcpyAsync(&R, qinc + N - 1, 4, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  h->R = R;
+  uint32_t *q_j0, *q_v, *q_doc;
+  EZ_ALLOC(h, q_j0, uint32_t, R);
+  EZ_ALLOC(h, q_v, uint32_t, R);
+  EZ_ALLOC(h, q_doc, uint32_t, R);
+  k_run_heads<<<blocks(N), 256, 0, s>>>(k_out, head, qinc, tw, N, q_j0, q_v, q_doc);
+  h->release(k_out);
+  h->release(head);
+  // ---- word-major run order (stable by word => docs ascending within a word)
+  uint32_t *q_iota, *rperm, *vs;
+  EZ_ALLOC(h, q_iota, uint32_t, R);
+  EZ_ALLOC(h, rperm, uint32_t, R);
+  EZ_ALLOC(h, vs, uint32_t, R);
+  k_iota<<<blocks(R), 256, 0, s>>>(q_iota, R);
+  int vbits = 1;
+  while (vbits < 32 && ((h->V - 1) >> vbits)) ++vbits;
+  st = cub_call(h, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, q_v, vs, q_iota, rperm, (int)R, 0, vbits, s);
+  });
+  if (st) return st;
+  h->release(q_iota);
+  h->release(q_v);
+  uint32_t *d_dofs, *run_j0, *run_dbase, *len32, *rid_of_q, *trid;
+  uint16_t* run_len;
+  EZ_ALLOC(h, d_dofs, uint32_t, h->Dn + 1);
+  EZ_CUDA(h, cudaMemcpyAsync(d_dofs, dofs.data(), sizeof(uint32_t) * (h->Dn + 1), cudaMemcpyHostToDevice, s));
+  EZ_ALLOC(h, run_j0, uint32_t, R);
+  EZ_ALLOC(h, run_dbase, uint32_t, R);
+  EZ_ALLOC(h, run_len, uint16_t, R);
+  EZ_ALLOC(h, len32, uint32_t, R + 1);
+  EZ_ALLOC(h, rid_of_q, uint32_t, R);
+  k_run_tables<<<blocks(R), 256, 0, s>>>(rperm, R, N, q_j0, q_doc, d_dofs, run_j0, run_dbase, run_len, len32, rid_of_q);
+  h->release(q_j0);
+  h->release(q_doc);
+  h->release(rperm);
+  EZ_ALLOC(h, trid, uint32_t, N);
+  k_trid<<<blocks(N), 256, 0, s>>>(qinc, rid_of_q, N, trid);
+  h->release(qinc);
+  h->release(rid_of_q);
+  // ---- items: per word, split dense words every split_threshold tokens
+  uint32_t *wrun, *tokpre, *ihead, *r_iota, *r0s, *d_ni;
+  EZ_ALLOC(h, wrun, uint32_t, h->V + 1);
+  k_wrun<<<blocks(h->V + 1), 256, 0, s>>>(vs, R, h->V, wrun);
+  EZ_ALLOC(h, tokpre, uint32_t, R + 1);
+  EZ_CUDA(h, cudaMemsetAsync(len32 + R, 0, 4, s));
+  st = cub_call(h, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, len32, tokpre, (int)(R + 1), s); });
+  if (st) return st;
+  h->release(len32);
+  const uint32_t split = o.split_threshold ? o.split_threshold : 10000u;
+  EZ_ALLOC(h, ihead, uint32_t, R);
+  k_item_heads<<<blocks(R), 256, 0, s>>>(vs, wrun, tokpre, R, h->Vd, split, ihead);
+  EZ_ALLOC(h, r_iota, uint32_t, R);
+  EZ_ALLOC(h, r0s, uint32_t, R);
+  EZ_ALLOC(h, d_ni, uint32_t, 1);
+  k_iota<<<blocks(R), 256, 0, s>>>(r_iota, R);
+  st = cub_call(h, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, r_iota, ihead, r0s, d_ni, (int)R, s);
+  });
+  if (st) return st;
+  uint32_t NI = 0;
+  EZ_CUDA(h, cudaMemcpyAsync(&NI, d_ni, 4, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  h->release(r_iota);
+  h->release(ihead);
+  uint32_t* item4;
+  EZ_ALLOC(h, item4, uint32_t, 4ull * NI);
+  k_items<<<blocks(NI), 256, 0, s>>>(r0s, NI, R, vs, tokpre, item4);
+  std::vector<uint32_t> it4(4ull * NI);
+  EZ_CUDA(h, cudaMemcpyAsync(it4.data(), item4, sizeof(uint32_t) * 4ull * NI, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  h->release(item4);
+  h->release(r0s);
+  h->release(d_ni);
+  h->release(vs);
+  h->release(tokpre);
+  h->release(wrun);
+  // heavy items first (the hardware block scheduler then balances the tail)
+  std::vector<uint32_t> order(NI);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return it4[4 * a + 3] > it4[4 * b + 3]; });
+  std::vector<uint32_t> iw(NI), ir0(NI), ir1(NI), int_(NI);
+  for (uint32_t i = 0; i < NI; ++i) {
+    const uint32_t q = order[i];
+    iw[i] = it4[4 * q];
+    ir0[i] = it4[4 * q + 1];
+    ir1[i] = it4[4 * q + 2];
+    int_[i] = it4[4 * q + 3];
+  }
+  h->n_items = NI;
+  uint32_t *item_word, *item_r0, *item_r1, *item_ntok;
+  EZ_ALLOC(h, item_word, uint32_t, NI);
+  EZ_ALLOC(h, item_r0, uint32_t, NI);
+  EZ_ALLOC(h, item_r1, uint32_t, NI);
+  EZ_ALLOC(h, item_ntok, uint32_t, NI);
+  EZ_CUDA(h, cudaMemcpyAsync(item_word, iw.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
+  EZ_CUDA(h, cudaMemcpyAsync(item_r0, ir0.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
+  EZ_CUDA(h, cudaMemcpyAsync(item_r1, ir1.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
+  EZ_CUDA(h, cudaMemcpyAsync(item_ntok, int_.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
+  // ---- doc tiers (static: L_d does not change)
+  std::vector<uint32_t> dw, db;
+  for (uint32_t d = 0; d < h->Dn; ++d) (L[d] <= 512 ? dw : db).push_back(d);
+  std::stable_sort(db.begin(), db.end(), [&](uint32_t a, uint32_t b) { return L[a] > L[b]; });
+  h->n_docs_w = (uint32_t)dw.size();
+  h->n_docs_b = (uint32_t)db.size();
+  EZ_ALLOC(h, h->docs_w, uint32_t, dw.size());
+  EZ_ALLOC(h, h->docs_b, uint32_t, db.size());
+  if (!dw.empty()) EZ_CUDA(h, cudaMemcpyAsync(h->docs_w, dw.data(), 4 * dw.size(), cudaMemcpyHostToDevice, s));
+  if (!db.empty()) EZ_CUDA(h, cudaMemcpyAsync(h->docs_b, db.data(), 4 * db.size(), cudaMemcpyHostToDevice, s));
+  // ---- remaining state
+  uint32_t *d_tofs, *d_wtok;
+  EZ_ALLOC(h, d_tofs, uint32_t, h->Vt + 1);
+  EZ_ALLOC(h, d_wtok, uint32_t, h->V + 1);
+  EZ_CUDA(h, cudaMemcpyAsync(d_tofs, tofs.data(), 4ull * (h->Vt + 1), cudaMemcpyHostToDevice, s));
+  EZ_CUDA(h, cudaMemcpyAsync(d_wtok, wtok.data(), 4ull * (h->V + 1), cudaMemcpyHostToDevice, s));
+  Dev& d = h->dev;
+  fill_dev(h);
+  d.dofs = d_dofs;
+  d.tw = tw;
+  d.trid = trid;
+  d.run_j0 = run_j0;
+  d.run_dbase = run_dbase;
+  d.run_len = run_len;
+  d.tofs = d_tofs;
+  d.wtok = d_wtok;
+  d.item_word = item_word;
+  d.item_r0 = item_r0;
+  d.item_r1 = item_r1;
+  d.item_ntok = item_ntok;
+  EZ_ALLOC(h, d.D, uint32_t, (size_t)N + 2ull * h->Dn);
+  EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
+  EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
+  EZ_ALLOC(h, d.den, double, h->K);
+  EZ_ALLOC(h, d.what0, double, h->K);
+  EZ_ALLOC(h, d.ctr, ezl::Counters, 1);
+  for (int b = 0; b < 2; ++b) {
+    Buf& B = h->buf[b];
+    EZ_ALLOC(h, B.z, uint16_t, N);
+    EZ_ALLOC(h, B.Wd, int32_t, (size_t)h->Vd * h->K);
+    EZ_ALLOC(h, B.Wt, uint32_t, h->tail_cap);
+    EZ_ALLOC(h, B.tnnz, uint32_t, std::max<uint32_t>(h->Vt, 1));
+    EZ_ALLOC(h, B.nk, int32_t, h->K);
+  }
+  EZ_CUDA(h, cudaMemsetAsync(d.rec, 0, sizeof(ezl::WordRec) * h->V, s));
+  EZ_ALLOC(h, h->llpt_partial, double, std::max<uint32_t>(NI, 1));
+  EZ_ALLOC(h, h->llpt_out, double, 1);
+  EZ_CUDA(h, cudaMallocHost(&h->ctr_host, sizeof(ezl::Counters) * ezlda::kSlots));
+  memset(h->ctr_host, 0, sizeof(ezl::Counters) * ezlda::kSlots);
+  h->slots.resize(ezlda::kSlots);
+  for (auto& sl : h->slots)
+    for (auto& e : sl.ev) EZ_CUDA(h, cudaEventCreate(&e));
+  h->release(d_newword);
+  h->release(d_L);
+  h->release(d_cnt);
+  h->release(d_max);
+  EZ_CUDA(h, ezl::configure_kernels(h->K));
+  // ---- iteration 0
+  h->cur = 0;
+  ezl::launch_init_topics(d, h->buf[0].z, s);
+  EZ_CUDA(h, cudaGetLastError());
+  if ((st = rebuild_counts(h))) return st;
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  h->iteration = 0;
+  return EZLDA_OK;
+}
+
+// Fold the oldest pending iteration record into `last` and `sum`.
+ezlda_status fold_one(ezlda* h) {
+  const int si = h->pending.front();
+  h->pending.erase(h->pending.begin());
+  ezlda::Slot& sl = h->slots[si];
+  EZ_CUDA(h, cudaEventSynchronize(sl.ev[4]));
+  ezlda_iter_stats st{};
+  const ezl::Counters& c = h->ctr_host[si];
+  st.iteration = sl.iteration;
+  st.n_tokens = h->N;
+  st.skip_S = c.skip_S;
+  st.skip_final = c.skip_S + c.skip_M;
+  st.sampled = c.sampled;
+  st.active_runs = c.active_runs;
+  st.drow_words = c.drow_words;
+  st.d_nnz = c.d_nnz;
+  st.kernel_launches = sl.launches;
+  if (h->timing) {
+    float a = 0, b = 0, cc = 0, dd = 0;
+    EZ_CUDA(h, cudaEventElapsedTime(&a, sl.ev[0], sl.ev[1]));
+    EZ_CUDA(h, cudaEventElapsedTime(&b, sl.ev[1], sl.ev[2]));
+    EZ_CUDA(h, cudaEventElapsedTime(&cc, sl.ev[2], sl.ev[3]));
+    EZ_CUDA(h, cudaEventElapsedTime(&dd, sl.ev[3], sl.ev[4]));
+    st.ms_wordprep = a;
+    st.ms_docpass = b;
+    st.ms_sample = cc;
+    st.ms_allreduce = dd;
+    st.ms_total = (double)a + b + cc + dd;
+  }
+  // DESIGN.md byte model (algorithmic bytes at payload granularity):
+  //   doc pass: per token z read 2 + tw 4 ; skipped token z write 2 ; failing token trid 4 ;
+  //             D rows written 4 (nnz + 2) per doc
+  //   sampler:  per active run 10 B of run table + D row 4 (nnz + 2) ; sampled token z write 2 ;
+  //             per item the staged W row (4 B x K)
+  //   word-prep: W rows read 4 B x Vd K (+ tail), W rebuilt 4 B x Vd K
+  const double N = (double)h->N;
+  const double tok_fail = N - (double)c.skip_S;
+  st.model_bytes_docpass = N * (2.0 + 4.0) + (double)c.skip_S * 2.0 + tok_fail * 4.0 +
+                           4.0 * ((double)c.d_nnz + 2.0 * h->Dn);
+  st.model_bytes_sample = (double)c.active_runs * 10.0 + 4.0 * (double)c.drow_words + (double)c.sampled * 2.0 +
+                          (double)h->n_items * 4.0 * h->K;
+  st.model_bytes = st.model_bytes_docpass + st.model_bytes_sample + 2.0 * 4.0 * (double)h->Vd * h->K;
+  h->last = st;
+  ezlda_iter_stats& S = h->sum;
+  S.ms_total += st.ms_total;
+  S.ms_wordprep += st.ms_wordprep;
+  S.ms_docpass += st.ms_docpass;
+  S.ms_sample += st.ms_sample;
+  S.ms_allreduce += st.ms_allreduce;
+  S.n_tokens += st.n_tokens;
+  S.skip_S += st.skip_S;
+  S.skip_final += st.skip_final;
+  S.sampled += st.sampled;
+  S.active_runs += st.active_runs;
+  S.drow_words += st.drow_words;
+  S.d_nnz += st.d_nnz;
+  S.model_bytes += st.model_bytes;
+  S.model_bytes_sample += st.model_bytes_sample;
+  S.model_bytes_docpass += st.model_bytes_docpass;
+  S.kernel_launches += st.kernel_launches;
+  h->sum_n += 1;
+  return EZLDA_OK;
+}
+
+ezlda_status fold_all(ezlda* h) {
+  while (!h->pending.empty()) {
+    ezlda_status st = fold_one(h);
+    if (st) return st;
+  }
+  return EZLDA_OK;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------
+// C ABI
+// ----------------------------------------------------------------------------
+extern "C" {
+
+ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uint64_t n_tokens, uint32_t n_docs,
+                          uint32_t V, uint32_t K, double alpha, double beta, uint64_t seed,
+                          const ezlda_options* opts, ezlda** out) {
+  g_create_error.clear();
+  if (out) *out = nullptr;
+  auto bad = [&](ezlda_status s, const char* m) {
+    g_create_error = m;
+    return s;
+  };
+  if (!out || !word_ids || !doc_ids) return bad(EZLDA_E_INVALID, "NULL argument");
+  if (n_tokens == 0 || K == 0 || V == 0 || n_docs == 0) return bad(EZLDA_E_INVALID, "n_tokens, K, V and n_docs must be > 0");
+  if (!(alpha > 0.0) || !(beta > 0.0)) return bad(EZLDA_E_INVALID, "alpha and beta must be > 0");
+  if (K > 65535) return bad(EZLDA_E_RANGE, "K > 65535 (16-bit topic packing, P:753)");
+  if (K > 16384) return bad(EZLDA_E_RANGE, "K > 16384 not supported by this build (NEXT-2)");
+  if (n_tokens >= (1ull << 32)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^32 per shard");
+  ezlda_options o{};
+  if (opts) o = *opts;
+  if (o.g > 3) return bad(EZLDA_E_INVALID, "g must be in {1,2,3} (0 = default 2)");
+  if (o.w_mode > 2) return bad(EZLDA_E_INVALID, "unknown w_mode");
+  ezlda* h = new (std::nothrow) ezlda();
+  if (!h) return bad(EZLDA_E_NOMEM, "host allocation failed");
+  h->N = n_tokens;
+  h->Dn = n_docs;
+  h->V = V;
+  h->K = K;
+  h->alpha = alpha;
+  h->beta = beta;
+  h->seed = seed;
+  h->g = o.g ? o.g : 2;
+  h->rank = o.rank;
+  h->world = o.world > 1 ? o.world : 1;
+  h->timing = !o.no_phase_timing;
+  h->dev.token_base = o.token_base;
+  ezlda_status st = EZLDA_OK;
+  if (o.stream) {
+    h->stream = (cudaStream_t)o.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      g_create_error = "cudaStreamCreate failed (no CUDA device?)";
+      delete h;
+      return EZLDA_E_CUDA;
+    }
+    h->own_stream = true;
+  }
+  if (h->world > 1) {
+    if (!o.nccl_unique_id || o.rank < 0 || o.rank >= h->world) {
+      st = h->fail(EZLDA_E_INVALID, "world > 1 needs nccl_unique_id and 0 <= rank < world");
+    } else if (!nccl().ok) {
+      st = h->fail(EZLDA_E_NCCL, "libnccl.so.2 could not be loaded");
+    } else {
+      ncclUniqueId id;
+      memcpy(&id, o.nccl_unique_id, sizeof(id));
+      ncclResult_t r = nccl().CommInitRank(&h->comm, h->world, id, h->rank);
+      if (r != ncclSuccess) st = h->fail(EZLDA_E_NCCL, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+    }
+  }
+  if (!st) st = do_create(h, word_ids, doc_ids, o);
+  if (st) {
+    g_create_error = h->err;
+    ezlda_destroy(h);
+    return st;
+  }
+  *out = h;
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
+  if (!h) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  cudaStream_t s = h->stream;
+  for (uint32_t it = 0; it < n_iters; ++it) {
+    const uint32_t i = h->iteration + 1;
+    Buf& cur = h->buf[h->cur];
+    Buf& nxt = h->buf[1 - h->cur];
+    if ((int)h->pending.size() == ezlda::kSlots) {
+      ezlda_status st = fold_one(h);
+      if (st) return st;
+    }
+    const int si = (int)(h->slot_counter++ % ezlda::kSlots);
+    ezlda::Slot& sl = h->slots[si];
+    cudaEvent_t* ev = sl.ev;
+    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[0], s));
+    EZ_CUDA(h, cudaMemsetAsync(h->dev.ctr, 0, sizeof(ezl::Counters), s));
+    EZ_CUDA(h, cudaMemsetAsync(h->dev.flags, 0, sizeof(uint32_t) * ((h->R + 31) / 32), s));
+    EZ_CUDA(h, cudaMemsetAsync(nxt.Wd, 0, sizeof(int32_t) * (size_t)h->Vd * h->K, s));
+    EZ_CUDA(h, cudaMemsetAsync(nxt.nk, 0, sizeof(int32_t) * h->K, s));
+    EZ_CUDA(h, cudaMemsetAsync(nxt.tnnz, 0, sizeof(uint32_t) * std::max<uint32_t>(h->Vt, 1), s));
+    ezl::launch_den(h->dev, cur, s);
+    ezl::launch_word_prep(h->dev, cur, s);
+    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
+    ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);
+    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
+    ezl::launch_sampler(h->dev, cur, nxt, h->n_items, i, false, s);
+    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
+    EZ_CUDA(h, cudaGetLastError());
+    ezlda_status st;
+    if ((st = allreduce(h, nxt.Wd, (size_t)h->Vd * h->K, ncclInt32))) return st;
+    if ((st = allreduce(h, nxt.nk, h->K, ncclInt32))) return st;
+    EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaEventRecord(ev[4], s));
+    sl.iteration = i;
+    sl.launches = 3u + (h->n_docs_w ? 1u : 0u) + (h->n_docs_b ? 1u : 0u) - (h->n_items ? 0u : 1u);
+    h->pending.push_back(si);
+    h->cur = 1 - h->cur;
+    h->iteration = i;
+    h->D_fresh = false;  // D rows describe z^{i-1}
+  }
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W, ezlda_csr* D) {
+  if (!h) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  cudaStream_t s = h->stream;
+  Buf& b = h->buf[h->cur];
+  if (topics) {
+    uint16_t* tmp = h->alloc<uint16_t>(h->N);
+    if (!tmp) return h->fail(EZLDA_E_NOMEM, "topics staging");
+    ezl::launch_topics_to_input(b.z, h->perm, (uint32_t)h->N, tmp, s);
+    EZ_CUDA(h, cudaGetLastError());
+    EZ_CUDA(h, cudaMemcpyAsync(topics, tmp, sizeof(uint16_t) * h->N, cudaMemcpyDefault, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    h->release(tmp);
+  }
+  if (n_k) {
+    EZ_CUDA(h, cudaMemcpyAsync(n_k, b.nk, sizeof(int32_t) * h->K, cudaMemcpyDefault, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+  }
+  if (W) {
+    std::vector<int32_t> Wd((size_t)h->Vd * h->K);
+    std::vector<uint32_t> Wt(h->tail_cap), tnnz(h->Vt), tofs(h->Vt + 1);
+    if (!Wd.empty()) EZ_CUDA(h, cudaMemcpyAsync(Wd.data(), b.Wd, 4 * Wd.size(), cudaMemcpyDeviceToHost, s));
+    if (!Wt.empty()) EZ_CUDA(h, cudaMemcpyAsync(Wt.data(), b.Wt, 4 * Wt.size(), cudaMemcpyDeviceToHost, s));
+    if (h->Vt) {
+      EZ_CUDA(h, cudaMemcpyAsync(tnnz.data(), b.tnnz, 4ull * h->Vt, cudaMemcpyDeviceToHost, s));
+      EZ_CUDA(h, cudaMemcpyAsync(tofs.data(), h->dev.tofs, 4ull * (h->Vt + 1), cudaMemcpyDeviceToHost, s));
+    }
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    const bool fill = W->col && W->val;
+    uint64_t nnz = 0;
+    W->rows = h->V;
+    for (uint32_t ov = 0; ov < h->V; ++ov) {
+      if (W->row_ptr) W->row_ptr[ov] = nnz;
+      const uint32_t v = h->newword[ov];
+      if (v < h->Vd) {
+        const int32_t* r = &Wd[(size_t)v * h->K];
+        for (uint32_t k = 0; k < h->K; ++k)
+          if (r[k]) {
+            if (fill) {
+              if (nnz >= W->nnz) return h->fail(EZLDA_E_INVALID, "W csr capacity too small");
+              W->col[nnz] = (uint16_t)k;
+              W->val[nnz] = r[k];
+            }
+            ++nnz;
+          }
+      } else {
+        const uint32_t t = v - h->Vd;
+        for (uint32_t e = 0; e < tnnz[t]; ++e) {
+          const uint32_t p = Wt[tofs[t] + e];
+          if (fill) {
+            if (nnz >= W->nnz) return h->fail(EZLDA_E_INVALID, "W csr capacity too small");
+            W->col[nnz] = (uint16_t)(p >> 16);
+            W->val[nnz] = (int32_t)(p & 0xFFFFu);
+          }
+          ++nnz;
+        }
+      }
+    }
+    if (W->row_ptr) W->row_ptr[h->V] = nnz;
+    W->nnz = nnz;
+  }
+  if (D) {
+    ezlda_status st = ensure_D(h);
+    if (st) return st;
+    std::vector<uint32_t> Dh(h->N + 2ull * h->Dn), dofs(h->Dn + 1);
+    EZ_CUDA(h, cudaMemcpyAsync(Dh.data(), h->dev.D, 4 * Dh.size(), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaMemcpyAsync(dofs.data(), h->dev.dofs, 4ull * (h->Dn + 1), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    const bool fill = D->col && D->val;
+    uint64_t nnz = 0;
+    D->rows = h->Dn;
+    for (uint32_t d = 0; d < h->Dn; ++d) {
+      if (D->row_ptr) D->row_ptr[d] = nnz;
+      const uint32_t base = dofs[d] + 2 * d;
+      const uint32_t n = (dofs[d + 1] > dofs[d]) ? (Dh[base] & 0xFFFFu) : 0u;
+      for (uint32_t e = 0; e < n; ++e) {
+        const uint32_t p = Dh[base + 2 + e];
+        if (fill) {
+          if (nnz >= D->nnz) return h->fail(EZLDA_E_INVALID, "D csr capacity too small");
+          D->col[nnz] = (uint16_t)(p >> 16);
+          D->val[nnz] = (int32_t)(p & 0xFFFFu);
+        }
+        ++nnz;
+      }
+    }
+    if (D->row_ptr) D->row_ptr[h->Dn] = nnz;
+    D->nnz = nnz;
+  }
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_set_topics(ezlda* h, const uint16_t* topics, uint32_t iterations_done) {
+  if (!h || !topics) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  std::vector<uint16_t> tmp_h;
+  cudaPointerAttributes attr{};
+  const bool on_dev = cudaPointerGetAttributes(&attr, topics) == cudaSuccess && attr.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  if (!on_dev) {
+    for (uint64_t t = 0; t < h->N; ++t)
+      if (topics[t] >= h->K) return h->fail(EZLDA_E_INVALID, "topic %u >= K at token %llu", topics[t], (unsigned long long)t);
+  }
+  uint16_t* tmp = h->alloc<uint16_t>(h->N);
+  if (!tmp) return h->fail(EZLDA_E_NOMEM, "topics staging");
+  EZ_CUDA(h, cudaMemcpyAsync(tmp, topics, sizeof(uint16_t) * h->N, cudaMemcpyDefault, h->stream));
+  ezl::launch_topics_from_input(tmp, h->perm, (uint32_t)h->N, h->buf[h->cur].z, h->stream);
+  EZ_CUDA(h, cudaGetLastError());
+  ezlda_status st = rebuild_counts(h);
+  if (st) return st;
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  h->release(tmp);
+  h->iteration = iterations_done;
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_loglik(ezlda* h, double* llpt) {
+  if (!h || !llpt) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  ezlda_status st = ensure_D(h);
+  if (st) return st;
+  Buf& b = h->buf[h->cur];
+  ezl::launch_den(h->dev, b, h->stream);
+  ezl::launch_llpt(h->dev, b, h->n_items, h->llpt_partial, h->llpt_out, h->stream);
+  EZ_CUDA(h, cudaGetLastError());
+  if ((st = allreduce(h, h->llpt_out, 1, ncclFloat64))) return st;
+  double sum = 0;
+  EZ_CUDA(h, cudaMemcpyAsync(&sum, h->llpt_out, 8, cudaMemcpyDeviceToHost, h->stream));
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  *llpt = sum / (double)h->N_global;
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_stats(const ezlda* hc, ezlda_iter_stats* last) {
+  ezlda* h = const_cast<ezlda*>(hc);
+  if (!h || !last) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  ezlda_status st = fold_all(h);
+  if (st) return st;
+  *last = h->last;
+  return EZLDA_OK;
+}
+
+ezlda_status ezlda_stats_sum(ezlda* h, ezlda_iter_stats* sum, int reset) {
+  if (!h || !sum) return EZLDA_E_INVALID;
+  if (h->sticky) return EZLDA_E_STATE;
+  ezlda_status st = fold_all(h);
+  if (st) return st;
+  *sum = h->sum;
+  sum->iteration = h->sum_n;
+  if (reset) {
+    h->sum = ezlda_iter_stats{};
+    h->sum_n = 0;
+  }
+  return EZLDA_OK;
+}
+
+const char* ezlda_last_error(const ezlda* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void ezlda_destroy(ezlda* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->allocs) cudaFree(p);
+  h->allocs.clear();
+  if (h->ctr_host) cudaFreeHost(h->ctr_host);
+  for (auto& sl : h->slots)
+    for (auto& e : sl.ev)
+      if (e) cudaEventDestroy(e);
+  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+size_t ezlda_nccl_id_size(void) { return sizeof(ncclUniqueId); }
+
+ezlda_status ezlda_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return EZLDA_E_INVALID;
+  if (!nccl().ok) return EZLDA_E_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return EZLDA_E_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return EZLDA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// kernels.h -- device state layout and kernel launchers of the ezLDA hot path.
+//
+// HBM layout (one shard; N tokens, Dn docs, R (doc, word) runs, V words, K topics):
+//   doc-major token arrays (j in [0, N), docs contiguous, tokens of a doc sorted by word):
+//     tw[j]   u32  relabelled word id (words ordered by count desc)
+//     trid[j] u32  index of the token's run in word-major run order
+//     z[2][j] u16  topics, double-buffered (snapshot semantics)
+//     perm[j] u32  input index of token j (output order only)
+//   dofs[Dn+1] u32 token offsets of docs; D rows at dbase(d) = dofs[d] + 2d:
+//     D[dbase] = (L_d << 16) | nnz_d, D[dbase+1] = dofs[d], D[dbase+2+i] = (topic << 16) | count
+//     sorted by topic (packed CSR; rebuilt every iteration)
+//   word-major runs r in [0, R) (runs of word v contiguous, docs ascending):
+//     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
+//   flags[R/32] u32: run r holds a token that failed the MPT skip test (L2 resident)
+//   W: dense rows int32 [Vd x K] for words v < Vd, packed sparse tail rows (capacity
+//     min(c_v, K) at tofs[v-Vd]) with tnnz[v-Vd]; double-buffered with n_k[K].
+//   rec[V] WordRec (48 B): top-4 topics/values and Q' of every word.
+//   items: (word, run range, tokens): the sampler's work list, heavy first.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace ezl {
+
+struct Counters {  // device-side per-iteration counters
+  unsigned long long skip_S, skip_M, sampled, active_runs, drow_words, d_nnz;
+};
+
+struct Dev {
+  // sizes and parameters
+  uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
+  double alpha, beta, Vbeta;
+  uint64_t seed, token_base;
+  // static structure
+  const uint32_t* dofs;
+  const uint32_t* tw;
+  const uint32_t* trid;
+  const uint32_t* run_j0;
+  const uint32_t* run_dbase;
+  const uint16_t* run_len;
+  const uint32_t* tofs;    // [V - Vd + 1] tail row offsets
+  const uint32_t* wtok;    // [V + 1] token offsets per word (relabelled ids)
+  const uint32_t* item_word;
+  const uint32_t* item_r0;
+  const uint32_t* item_r1;
+  const uint32_t* item_ntok;
+  // dynamic state
+  uint32_t* D;
+  uint32_t* flags;
+  WordRec* rec;
+  double* den;    // [K] n_k + V beta
+  double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
+  Counters* ctr;
+};
+
+// Double-buffered pieces of the state.
+struct Buf {
+  uint16_t* z;
+  int32_t* Wd;      // dense rows [Vd * K]
+  uint32_t* Wt;     // tail packed rows
+  uint32_t* tnnz;   // [V - Vd]
+  int32_t* nk;      // [K]
+};
+
+// ----- per-iteration kernels -----
+void launch_den(const Dev& d, const Buf& cur, cudaStream_t s);
+void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s);
+// doc pass over the two length tiers; skip_test=false only rebuilds D (for counts/loglik)
+void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_t* docs_w, uint32_t n_w,
+                     const uint32_t* docs_b, uint32_t n_b, uint32_t iteration, bool skip_test, cudaStream_t s);
+// sampler over items; count_only=true rebuilds W/n_k of `cur.z` into `nxt` (init, set_topics)
+void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
+                    bool count_only, cudaStream_t s);
+void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s);
+
+// ----- setup / IO kernels -----
+void launch_init_topics(const Dev& d, uint16_t* z, cudaStream_t s);
+void launch_topics_to_input(const uint16_t* z, const uint32_t* perm, uint32_t N, uint16_t* out, cudaStream_t s);
+void launch_topics_from_input(const uint16_t* in, const uint32_t* perm, uint32_t N, uint16_t* z, cudaStream_t s);
+
+size_t sampler_smem_bytes(uint32_t K);
+size_t word_prep_smem_bytes(uint32_t K);
+size_t doc_block_smem_bytes(uint32_t K);
+cudaError_t configure_kernels(uint32_t K);
+
+}  // namespace ezl

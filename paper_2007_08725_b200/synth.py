@@ -128,7 +128,7 @@ def planted_corpus_torch(n_docs: int, V: int, mean_len: float, sigma: float, K_t
     n = int(L.sum().item())
     doc_ids = torch.repeat_interleave(torch.arange(n_docs, device=device, dtype=torch.int32), L)
     z = torch.empty(n, device=device, dtype=torch.int32)
-    chunk = 1 << 26
+    chunk = 1 << 22
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
         d = doc_ids[s:e].long()

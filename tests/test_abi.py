@@ -1,0 +1,75 @@
+"""CPU checks of the C-ABI boundary: the library loads, exports every symbol that
+include/ezlda.h declares, and the ctypes mirrors of the ABI structs match the C
+layout (compiled from the header with gcc).  No compute call is made here."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ezlda.h")
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_2007_08725_b200 import build
+
+    return build.build()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ezlda_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_the_call_set():
+    f = declared_functions()
+    for name in ("ezlda_create", "ezlda_iterate", "ezlda_counts", "ezlda_loglik", "ezlda_stats", "ezlda_destroy"):
+        assert name in f
+
+
+def test_library_exports_every_declared_symbol(lib_path):
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib_path], text=True)
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+
+
+def test_library_loads_and_binding_covers_header(lib_path):
+    from paper_2007_08725_b200 import lda
+
+    L = lda.load()
+    for name in declared_functions():
+        assert hasattr(L, name)
+    assert sorted(lda.EXPORTS) == declared_functions()
+    assert L.ezlda_nccl_id_size() == 128
+
+
+def test_struct_layout_matches_header(tmp_path):
+    import ctypes
+
+    from paper_2007_08725_b200 import lda
+
+    c = tmp_path / "sz.c"
+    c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ezlda.h"\n'
+                 'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(ezlda_options), sizeof(ezlda_csr),'
+                 ' sizeof(ezlda_iter_stats), offsetof(ezlda_options, token_base), offsetof(ezlda_iter_stats, model_bytes));'
+                 'return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)], text=True).split()]
+    assert got == [ctypes.sizeof(lda.Options), ctypes.sizeof(lda.CSR), ctypes.sizeof(lda.IterStats),
+                   lda.Options.token_base.offset, lda.IterStats.model_bytes.offset]
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2007_08725_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                code = re.sub(r"(#|//).*", "", txt)
+                code = re.sub(r'""".*?"""', "", code, flags=re.S)
+                assert "import oracle" not in code and "from oracle" not in code and "ezlda_oracle" not in code, fn

@@ -1,0 +1,255 @@
+"""GPU (CUDA path through the C ABI) vs the CPU oracle, element by element.
+
+One-step parity (BASELINE.json north star): every iteration the oracle is fed the
+GPU's z^{i-1}; both run iteration i with the same Philox stream; topics must agree
+on >= 99.99% of tokens, every disagreement must sit within 1e-12 Z of a bucket
+boundary (fp64 summation-order rounding), and the GPU's
+integer D / W / n_k must equal a brute-force recount of its own topics bit for bit.
+"""
+import numpy as np
+import pytest
+
+from paper_2007_08725_b200.synth import SAMPLER_SEED, planted_corpus_np
+
+pytestmark = pytest.mark.gpu
+
+TINY = dict(n_docs=100, V=500, mean_len=100.0, sigma=0.5)
+SMALL = dict(n_docs=2000, V=5000, mean_len=90.0, sigma=0.5)
+
+
+@pytest.fixture(scope="module")
+def ez():
+    from paper_2007_08725_b200 import lda
+
+    lda.load()
+    return lda
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return planted_corpus_np(**TINY)
+
+
+@pytest.fixture(scope="module")
+def small():
+    return planted_corpus_np(**SMALL)
+
+
+def brute(w, d, z, n_docs, V, K):
+    D = np.zeros((n_docs, K), np.int64)
+    W = np.zeros((V, K), np.int64)
+    np.add.at(D, (d.astype(np.int64), z.astype(np.int64)), 1)
+    np.add.at(W, (w.astype(np.int64), z.astype(np.int64)), 1)
+    return D, W
+
+
+def check_counts(ez, g, w, d, n_docs, V, K, z=None):
+    z = g.topics() if z is None else z
+    D, W = brute(w, d, z, n_docs, V, K)
+    Wg = ez.EzLDA.csr_to_dense(*g.W_csr(), K)
+    Dg = ez.EzLDA.csr_to_dense(*g.D_csr(), K)
+    assert np.array_equal(Wg, W), "W differs from recount"
+    assert np.array_equal(Dg, D), "D differs from recount"
+    assert np.array_equal(g.n_k(), W.sum(0)), "n_k differs from recount"
+    # packed rows are sorted by topic (CSR columns ascending within a row)
+    rp, col, _ = g.D_csr()
+    for r in range(0, n_docs, max(1, n_docs // 50)):
+        c = col[rp[r]:rp[r + 1]]
+        assert np.all(np.diff(c.astype(np.int64)) > 0)
+
+
+def boundary_distance(oracle_mod, orc, w, d, z_prev, t, K, alpha, g, it):
+    """Distance (relative to Z) from the token's x = u Z to the nearest breakpoint of
+    the [M | S' | Q'] layout, computed by the oracle on the snapshot z_prev."""
+    D, _, _ = orc.counts()
+    Drow = D[d[t]]
+    What = orc.what(int(w[t]))
+    u = oracle_mod.uniform(SAMPLER_SEED, it, int(orc.token_index()[t]))
+    det = oracle_mod.draw_three_branch(Drow, What, alpha, g, u)
+    K1 = det["K_sel"][0]
+    thr_gap = abs(u - det["thr"])
+    Wp = What.copy()
+    Wp[K1] = 0.0
+    Sp = np.cumsum(np.where(Drow > 0, Drow * Wp, 0.0))
+    Z = det["M"] + Sp[-1] + det["Qp"]
+    x = u * Z
+    bps = np.concatenate([[det["M"]], det["M"] + Sp, det["M"] + Sp[-1] + alpha * np.cumsum(Wp)])
+    return min(np.min(np.abs(bps - x)) / Z, thr_gap)
+
+
+def run_one_step_parity(ez, oracle_mod, w, d, n_docs, V, K, iters, g=2, check_every=1, **kw):
+    gpu = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, g=g, **kw)
+    orc = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, g=g)
+    z = gpu.topics()
+    assert np.array_equal(z, orc.topics()), "iteration-0 topics differ (Philox init)"
+    check_counts(ez, gpu, w, d, n_docs, V, K, z)
+    worst = 1.0
+    total_mismatch = 0
+    for i in range(1, iters + 1):
+        orc.set_topics(z, i - 1)
+        orc.iterate(1)
+        gpu.iterate(1)
+        zg, zo = gpu.topics(), orc.topics()
+        mism = np.nonzero(zg != zo)[0]
+        agree = 1.0 - len(mism) / len(zg)
+        worst = min(worst, agree)
+        total_mismatch += len(mism)
+        assert agree >= 0.9999, (i, len(mism))
+        if len(mism):
+            ref = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, g=g)
+            ref.set_topics(z, i - 1)
+            for t in mism[:20]:
+                dist = boundary_distance(oracle_mod, ref, w, d, z, int(t), K, gpu.alpha, g, i)
+                print(f"iteration {i} token {t}: gpu {zg[t]} oracle {zo[t]} boundary distance {dist:.3e} Z")
+                assert dist <= 1e-12, (i, t, dist)
+        st = gpu.stats()
+        so = orc.last_stats()
+        assert st["iteration"] == i
+        if not len(mism):
+            assert st["skip_S"] == so["skip_S"], (i, st["skip_S"], so["skip_S"])
+            assert st["skip_final"] == so["skip_final"], (i, st["skip_final"], so["skip_final"])
+            assert st["sampled"] == len(zg) - so["skip_S"]
+        if i % check_every == 0 or i == iters:
+            check_counts(ez, gpu, w, d, n_docs, V, K, zg)
+        z = zg
+    print(f"worst per-iteration agreement {worst:.6f}, total mismatches {total_mismatch}")
+    return gpu, orc
+
+
+def test_one_step_parity_tiny_50_iterations(ez, oracle_mod, tiny):
+    w, d = tiny
+    run_one_step_parity(ez, oracle_mod, w, d, TINY["n_docs"], TINY["V"], 16, 50, check_every=5)
+
+
+def test_one_step_parity_small(ez, oracle_mod, small):
+    w, d = small
+    run_one_step_parity(ez, oracle_mod, w, d, SMALL["n_docs"], SMALL["V"], 64, 8, check_every=4)
+
+
+@pytest.mark.parametrize("g", [1, 3])
+def test_one_step_parity_g(ez, oracle_mod, tiny, g):
+    w, d = tiny
+    run_one_step_parity(ez, oracle_mod, w, d, TINY["n_docs"], TINY["V"], 16, 6, g=g, check_every=3)
+
+
+def test_long_docs_block_tier_and_large_rows(ez, oracle_mod):
+    """Docs longer than 512 tokens (block tier of the doc pass), D rows with > 128 nonzeros
+    (register-spill path of the S' descent), K not a multiple of 32."""
+    w, d = planted_corpus_np(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5)
+    run_one_step_parity(ez, oracle_mod, w, d, 60, 3000, 1000, 4, check_every=2)
+
+
+def test_chain_parity_llpt_100_iterations(ez, oracle_mod, tiny):
+    """Independent 100-iteration chains: LLPT within 1e-3 relative (expected identical)."""
+    w, d = tiny
+    gpu = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED)
+    orc = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED)
+    gpu.iterate(100)
+    orc.iterate(100)
+    lg, lo = gpu.loglik(), orc.loglik(1)
+    print("LLPT gpu", lg, "oracle", lo, "topic agreement", np.mean(gpu.topics() == orc.topics()))
+    assert abs(lg - lo) <= 1e-3 * abs(lo)
+
+
+def test_llpt_parity_and_set_topics(ez, oracle_mod, small):
+    w, d = small
+    K = 64
+    gpu = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], K, seed=SAMPLER_SEED)
+    orc = oracle_mod.OracleLDA(w, d, SMALL["n_docs"], SMALL["V"], K, seed=SAMPLER_SEED)
+    for it in (0, 3):
+        if it:
+            gpu.iterate(it)
+        z = gpu.topics()
+        orc.set_topics(z, gpu.stats()["iteration"] if it else 0)
+        lg, lo = gpu.loglik(), orc.loglik(1)
+        assert abs(lg - lo) <= 1e-10 * abs(lo), (lg, lo)
+    # set_topics: arbitrary state, GPU rebuilds W / n_k; loglik matches
+    rng = np.random.default_rng(3)
+    z = rng.integers(0, K, size=len(w)).astype(np.uint16)
+    gpu.set_topics(z, 7)
+    assert np.array_equal(gpu.topics(), z)
+    check_counts(ez, gpu, w, d, SMALL["n_docs"], SMALL["V"], K, z)
+    orc.set_topics(z, 7)
+    assert abs(gpu.loglik() - orc.loglik(1)) <= 1e-10 * abs(orc.loglik(1))
+    gpu.iterate(1)
+    orc.iterate(1)
+    assert np.mean(gpu.topics() == orc.topics()) >= 0.9999
+
+
+def test_appendix_a_state_loglik(ez):
+    app = [(0, 0, 2), (0, 2, 1), (1, 1, 1), (1, 2, 0), (2, 0, 1), (2, 2, 3), (3, 1, 0)]
+    w = np.array([t[0] for t in app], np.uint32)
+    d = np.array([t[1] for t in app], np.uint32)
+    g = ez.EzLDA(w, d, 3, 4, 4, alpha=16.7, beta=0.01)
+    g.set_topics(np.array([t[2] for t in app], np.uint16), 0)
+    assert abs(g.loglik() - (-1.963006)) < 1e-6
+
+
+@pytest.mark.parametrize("knobs", [
+    dict(w_mode=1), dict(w_mode=2), dict(dense_threshold=3), dict(split_threshold=64),
+    dict(split_threshold=64, w_mode=1), dict(g=1), dict(g=3),
+])
+def test_knob_invariance(ez, tiny, knobs):
+    """Dense threshold, W mode, region split and g change speed only: T bit-identical."""
+    w, d = tiny
+    ref = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED)
+    alt = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED, **knobs)
+    for _ in range(6):
+        ref.iterate(1)
+        alt.iterate(1)
+        assert np.array_equal(ref.topics(), alt.topics()), knobs
+    assert np.array_equal(ref.n_k(), alt.n_k())
+
+
+def test_determinism(ez, small):
+    w, d = small
+    a = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], 64, seed=11)
+    b = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], 64, seed=11)
+    a.iterate(5)
+    b.iterate(5)
+    assert np.array_equal(a.topics(), b.topics())
+    assert a.loglik() == b.loglik()
+
+
+def test_input_order_and_empty_docs(ez, oracle_mod):
+    """Tokens not grouped by doc, empty docs, absent words: same topics as the oracle."""
+    rng = np.random.default_rng(8)
+    w, d = planted_corpus_np(n_docs=80, V=400, mean_len=60.0, sigma=0.7, seed=9)
+    d = d * 2  # odd doc ids are empty
+    perm = rng.permutation(len(w))
+    w, d = w[perm], d[perm]
+    V = 450  # words 400..449 never occur
+    gpu = ez.EzLDA(w, d, 161, V, 12, seed=4)
+    orc = oracle_mod.OracleLDA(w, d, 161, V, 12, seed=4)
+    for _ in range(5):
+        gpu.iterate(1)
+        orc.iterate(1)
+        assert np.mean(gpu.topics() == orc.topics()) >= 0.9999
+    check_counts(ez, gpu, w, d, 161, V, 12)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_degenerate_K(ez, oracle_mod, tiny, K):
+    w, d = tiny
+    run_one_step_parity(ez, oracle_mod, w, d, TINY["n_docs"], TINY["V"], K, 3)
+
+
+def test_single_token(ez):
+    g = ez.EzLDA(np.array([0], np.uint32), np.array([0], np.uint32), 1, 1, 1, alpha=50.0)
+    g.iterate(2)
+    assert g.topics()[0] == 0
+    assert g.loglik() == 0.0
+
+
+def test_invalid_arguments(ez):
+    w = np.array([0, 1], np.uint32)
+    d = np.array([0, 0], np.uint32)
+    with pytest.raises(ez.EzLDAError, match="E_INVALID"):
+        ez.EzLDA(w, d, 1, 1, 4)  # word id 1 >= V
+    with pytest.raises(ez.EzLDAError, match="E_INVALID"):
+        ez.EzLDA(w, d, 1, 2, 4, alpha=0.0)
+    with pytest.raises(ez.EzLDAError, match="E_RANGE"):
+        ez.EzLDA(w, d, 1, 2, 70000)
+    long_doc = np.zeros(70000, np.uint32)
+    with pytest.raises(ez.EzLDAError, match="E_RANGE"):
+        ez.EzLDA(long_doc, long_doc, 1, 1, 4)
