@@ -114,7 +114,7 @@ __global__ void k_iota(uint32_t* a, uint32_t n) {
 
 // word-major run tables from the sorted run permutation
 __global__ void k_run_tables(const uint32_t* rperm, uint32_t R, uint32_t N, const uint32_t* q_j0, const uint32_t* q_doc,
-                             const uint32_t* dofs, uint32_t* run_j0, uint32_t* run_dbase, uint16_t* run_len,
+                             const uint32_t* ddb, uint32_t* run_j0, uint32_t* run_dbase, uint16_t* run_len,
                              uint32_t* len32, uint32_t* rid_of_q) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < R) {
@@ -123,7 +123,7 @@ __global__ void k_run_tables(const uint32_t* rperm, uint32_t R, uint32_t N, cons
     const uint32_t j1 = (q + 1 < R) ? q_j0[q + 1] : N;
     const uint32_t d = q_doc[q];
     run_j0[r] = j0;
-    run_dbase[r] = dofs[d] + 2u * d;
+    run_dbase[r] = ddb[d];
     run_len[r] = (uint16_t)(j1 - j0);
     len32[r] = j1 - j0;
     rid_of_q[q] = r;
@@ -193,6 +193,7 @@ struct ezlda {
   uint32_t Dn = 0, V = 0, K = 0, R = 0, Vd = 0, Vt = 0;
   uint32_t n_items = 0, n_docs_w = 0, n_docs_b = 0;
   uint64_t tail_cap = 0;
+  uint64_t Dwords = 0;
   double alpha = 0, beta = 0;
   uint64_t seed = 0;
   uint32_t g = 2;
@@ -370,7 +371,15 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     if (L[d] > 65535) return h->fail(EZLDA_E_RANGE, "doc %u has %u tokens (> 65535, P:753)", d, L[d]);
   std::vector<uint32_t> dofs(h->Dn + 1, 0);
   for (uint32_t d = 0; d < h->Dn; ++d) dofs[d + 1] = dofs[d] + L[d];
-  if ((uint64_t)N + 2ull * h->Dn >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "tokens + 2 docs >= 2^32 per shard");
+  // D rows: 2 header words + L_d entries, padded to 16 bytes (TMA bulk-copy granularity)
+  std::vector<uint32_t> ddb(h->Dn);
+  uint64_t dwords = 0;
+  for (uint32_t d = 0; d < h->Dn; ++d) {
+    ddb[d] = (uint32_t)dwords;
+    dwords += ((uint64_t)L[d] + ezl::kDHdr + 3) & ~3ull;
+  }
+  if (dwords >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "D storage >= 2^32 words per shard");
+  h->Dwords = dwords;
   // global word counts (the dense/tail split and relabelling must agree on all ranks)
   std::vector<uint64_t> cnt(h->V);
   for (uint32_t v = 0; v < h->V; ++v) cnt[v] = cnt_local[v];
@@ -472,16 +481,18 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   if (st) return st;
   h->release(q_iota);
   h->release(q_v);
-  uint32_t *d_dofs, *run_j0, *run_dbase, *len32, *rid_of_q, *trid;
+  uint32_t *d_dofs, *d_ddb, *run_j0, *run_dbase, *len32, *rid_of_q, *trid;
   uint16_t* run_len;
   EZ_ALLOC(h, d_dofs, uint32_t, h->Dn + 1);
   EZ_CUDA(h, cudaMemcpyAsync(d_dofs, dofs.data(), sizeof(uint32_t) * (h->Dn + 1), cudaMemcpyHostToDevice, s));
+  EZ_ALLOC(h, d_ddb, uint32_t, h->Dn);
+  EZ_CUDA(h, cudaMemcpyAsync(d_ddb, ddb.data(), sizeof(uint32_t) * h->Dn, cudaMemcpyHostToDevice, s));
   EZ_ALLOC(h, run_j0, uint32_t, R);
   EZ_ALLOC(h, run_dbase, uint32_t, R);
   EZ_ALLOC(h, run_len, uint16_t, R);
   EZ_ALLOC(h, len32, uint32_t, R + 1);
   EZ_ALLOC(h, rid_of_q, uint32_t, R);
-  k_run_tables<<<blocks(R), 256, 0, s>>>(rperm, R, N, q_j0, q_doc, d_dofs, run_j0, run_dbase, run_len, len32, rid_of_q);
+  k_run_tables<<<blocks(R), 256, 0, s>>>(rperm, R, N, q_j0, q_doc, d_ddb, run_j0, run_dbase, run_len, len32, rid_of_q);
   h->release(q_j0);
   h->release(q_doc);
   h->release(rperm);
@@ -567,6 +578,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   Dev& d = h->dev;
   fill_dev(h);
   d.dofs = d_dofs;
+  d.ddb = d_ddb;
   d.tw = tw;
   d.trid = trid;
   d.run_j0 = run_j0;
@@ -578,7 +590,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   d.item_r0 = item_r0;
   d.item_r1 = item_r1;
   d.item_ntok = item_ntok;
-  EZ_ALLOC(h, d.D, uint32_t, (size_t)N + 2ull * h->Dn);
+  EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
   EZ_ALLOC(h, d.den, double, h->K);
@@ -646,14 +658,14 @@ ezlda_status fold_one(ezlda* h) {
   }
   // DESIGN.md byte model (algorithmic bytes at payload granularity):
   //   doc pass: per token z read 2 + tw 4 ; skipped token z write 2 ; failing token trid 4 ;
-  //             D rows written 4 (nnz + 2) per doc
-  //   sampler:  per active run 10 B of run table + D row 4 (nnz + 2) ; sampled token z write 2 ;
+  //             D rows written 4 (nnz + 4) per doc
+  //   sampler:  per active run 10 B of run table + D row 4 (nnz + 4) ; sampled token z write 2 ;
   //             per item the staged W row (4 B x K)
   //   word-prep: W rows read 4 B x Vd K (+ tail), W rebuilt 4 B x Vd K
   const double N = (double)h->N;
   const double tok_fail = N - (double)c.skip_S;
   st.model_bytes_docpass = N * (2.0 + 4.0) + (double)c.skip_S * 2.0 + tok_fail * 4.0 +
-                           4.0 * ((double)c.d_nnz + 2.0 * h->Dn);
+                           4.0 * ((double)c.d_nnz + 4.0 * h->Dn);
   st.model_bytes_sample = (double)c.active_runs * 10.0 + 4.0 * (double)c.drow_words + (double)c.sampled * 2.0 +
                           (double)h->n_items * 4.0 * h->K;
   st.model_bytes = st.model_bytes_docpass + st.model_bytes_sample + 2.0 * 4.0 * (double)h->Vd * h->K;
@@ -868,19 +880,20 @@ ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W
   if (D) {
     ezlda_status st = ensure_D(h);
     if (st) return st;
-    std::vector<uint32_t> Dh(h->N + 2ull * h->Dn), dofs(h->Dn + 1);
+    std::vector<uint32_t> Dh(h->Dwords), dofs(h->Dn + 1), ddb(h->Dn);
     EZ_CUDA(h, cudaMemcpyAsync(Dh.data(), h->dev.D, 4 * Dh.size(), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaMemcpyAsync(dofs.data(), h->dev.dofs, 4ull * (h->Dn + 1), cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaMemcpyAsync(ddb.data(), h->dev.ddb, 4ull * h->Dn, cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaStreamSynchronize(s));
     const bool fill = D->col && D->val;
     uint64_t nnz = 0;
     D->rows = h->Dn;
     for (uint32_t d = 0; d < h->Dn; ++d) {
       if (D->row_ptr) D->row_ptr[d] = nnz;
-      const uint32_t base = dofs[d] + 2 * d;
+      const uint32_t base = ddb[d];
       const uint32_t n = (dofs[d + 1] > dofs[d]) ? (Dh[base] & 0xFFFFu) : 0u;
       for (uint32_t e = 0; e < n; ++e) {
-        const uint32_t p = Dh[base + 2 + e];
+        const uint32_t p = Dh[base + ezl::kDHdr + e];
         if (fill) {
           if (nnz >= D->nnz) return h->fail(EZLDA_E_INVALID, "D csr capacity too small");
           D->col[nnz] = (uint16_t)(p >> 16);

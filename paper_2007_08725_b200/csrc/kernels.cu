@@ -13,6 +13,7 @@
 //                [M | S' | Q'] layout, then rebuild W and n_k from the item's
 //                histogram (skipped tokens count at K1)                         (P:546 steps 4-6,
 //                                                                                  P:822-846)
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.h"
@@ -21,7 +22,6 @@ namespace ezl {
 
 namespace {
 
-constexpr int kDrowCap = 1024;   // D-row entries staged per sampler warp (4 KB)
 constexpr int kDocWarpCap = 512; // doc-pass warp tier: documents up to 512 tokens
 constexpr int kDocWarps = 8;
 constexpr int kSampWarps = 8;
@@ -58,14 +58,19 @@ __device__ void stage_row(const Dev& d, const Buf& b, uint32_t v, double* row) {
   __syncthreads();
 }
 
-// Chunked prefix of a staged row: T[c] = warp-scan total of chunk c (32 entries),
-// CP[0] = 0, CP[c+1] = CP[c] + T[c] sequentially.  P(k) := CP[k/32] + scan_c(k%32).
-// Used identically by word-prep (Q'), the sampler (Q' descent) and LLPT.
+// Chunked prefix of a staged row (the Q' tree of P:384/P:400 in the order this
+// implementation fixes): T[c] = sequential sum of the 32 entries of chunk c,
+// CP[0] = 0, CP[c+1] = CP[c] + T[c] sequentially, and
+//   P(k) := CP[k/32] + (sequential sum of row[32 (k/32) .. k]),
+// which a single thread can evaluate (binary search over CP, then a walk of <= 32
+// entries).  Used identically by word-prep (Q' = alpha CP[nch]), the sampler (Q'
+// descent) and LLPT.
 __device__ void chunk_prefix(const double* row, uint32_t nch, double* T, double* CP) {
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (uint32_t c = warp; c < nch; c += nw) {
-    const double s = warp_incl_scan(row[c * 32 + lane]);
-    if (lane == 31) T[c] = s;
+  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (uint32_t t = 0; t < 32; ++t) acc = acc + row[c * 32 + t];
+    T[c] = acc;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -174,7 +179,6 @@ __global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
   double* CP = T + d.nch;
   __shared__ double s_v[4][4];
   __shared__ uint32_t s_k[4][4];
-  __shared__ uint32_t s_K1;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   stage_row(d, cur, v, row);
   Top4 t;
@@ -199,7 +203,6 @@ __global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
     }
     r.Qp = 0.0;
     d.rec[v] = r;
-    s_K1 = r.K[0];
     row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
   }
   __syncthreads();
@@ -245,6 +248,63 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
   }
 }
 
+// Warp tier, K <= 4096: one warp per doc with a private dense shared-memory histogram
+// (two 16-bit counters per word), C_j read straight from it, then an ordered
+// compaction over K that writes the packed D row and re-zeroes the counters.
+template <bool kSkipTest>
+__global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
+                                                              uint32_t n_docs, uint32_t iter) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t hw = d.Kpad >> 1;  // counter words per warp
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * hw;
+  for (uint32_t i = lane; i < hw; i += 32) hist[i] = 0;
+  __syncwarp();
+  unsigned long long n_skip = 0, n_nnz = 0;
+  for (uint32_t idx = blockIdx.x * kDocWarps + warp; idx < n_docs; idx += gridDim.x * kDocWarps) {
+    const uint32_t doc = docs[idx];
+    const uint32_t j0 = d.dofs[doc];
+    const uint32_t L = d.dofs[doc + 1] - j0;
+    for (uint32_t i = lane; i < L; i += 32) {
+      const uint32_t k = cur.z[j0 + i];
+      atomicAdd(&hist[k >> 1], 1u << ((k & 1u) << 4));
+    }
+    __syncwarp();
+    if (kSkipTest) {
+      doc_tokens_skip_test(d, nxt, j0, L, iter, lane, 32,
+                           [&](uint32_t k) { return (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu; }, n_skip);
+      __syncwarp();
+    }
+    uint32_t* Drow = d.D + d.ddb[doc];
+    uint32_t nnz = 0;
+    for (uint32_t base = 0; base < hw; base += 32) {
+      const uint32_t w = base + lane;
+      const uint32_t x = (w < hw) ? hist[w] : 0u;
+      const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
+      const uint32_t mlo = __ballot_sync(kFull, lo != 0), mhi = __ballot_sync(kFull, hi != 0);
+      const uint32_t lt = lanemask_lt();
+      const uint32_t pos = nnz + __popc(mlo & lt) + __popc(mhi & lt);
+      if (lo) Drow[kDHdr + pos] = ((2u * w) << 16) | lo;
+      if (hi) Drow[kDHdr + pos + (lo != 0)] = ((2u * w + 1u) << 16) | hi;
+      if (x) hist[w] = 0;
+      nnz += __popc(mlo) + __popc(mhi);
+    }
+    if (lane == 0) {
+      Drow[0] = (L << 16) | nnz;
+      Drow[1] = j0;
+    }
+    n_nnz += nnz;
+    __syncwarp();
+  }
+  n_skip = warp_sum(n_skip);
+  if (lane == 0) {
+    atomicAdd(&d.ctr->d_nnz, n_nnz);
+    if (kSkipTest) atomicAdd(&d.ctr->skip_S, n_skip);
+  }
+}
+
+// Warp tier, K > 4096: topics sorted by a bitonic network in shared memory, then
+// run-length encoded.
 template <bool kSkipTest>
 __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
                                                               uint32_t n_docs, uint32_t iter) {
@@ -258,7 +318,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf
   const uint32_t doc = docs[idx];
   const uint32_t j0 = d.dofs[doc];
   const uint32_t L = d.dofs[doc + 1] - j0;
-  const uint32_t dbase = j0 + 2u * doc;
+  const uint32_t dbase = d.ddb[doc];
   uint16_t* buf = s_key[warp];
   uint32_t P2 = 32;
   while (P2 < L) P2 <<= 1;
@@ -299,7 +359,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf
     const uint32_t s1 = (p + 1 < nnz) ? (uint32_t)ust[p + 1] : L;
     const uint32_t cnt = s1 - s0;
     ucnt[p] = (uint16_t)cnt;
-    Drow[2 + p] = ((uint32_t)ukey[p] << 16) | cnt;
+    Drow[kDHdr + p] = ((uint32_t)ukey[p] << 16) | cnt;
   }
   if (lane == 0) {
     Drow[0] = (L << 16) | nnz;
@@ -330,14 +390,14 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
   const uint32_t doc = docs[blockIdx.x];
   const uint32_t j0 = d.dofs[doc];
   const uint32_t L = d.dofs[doc + 1] - j0;
-  const uint32_t dbase = j0 + 2u * doc;
+  const uint32_t dbase = d.ddb[doc];
   for (uint32_t k = tid; k < d.Kpad; k += nt) hist[k] = 0;
   if (tid == 0) s_skip = 0;
   __syncthreads();
   for (uint32_t i = tid; i < L; i += nt) atomicAdd(&hist[cur.z[j0 + i]], 1u);
   __syncthreads();
   uint32_t* Drow = d.D + dbase;
-  const uint32_t nnz = block_compact(hist, d.K, Drow + 2, s_wsum, &s_run);
+  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run);
   if (tid == 0) {
     Drow[0] = (L << 16) | nnz;
     Drow[1] = j0;
@@ -360,169 +420,198 @@ struct RunCounters {
   uint32_t sampled, hitM, runs, words;
 };
 
-// Warp-cooperative processing of one flagged run (doc d, word v), P:546 steps 4-6:
-// the D row is read once (staged in this warp's shared buffer), each lane takes a
-// contiguous block of B entries (ascending topic order) and sums D[d][k] What'[v][k]
-// sequentially, one warp scan turns the 32 block sums into block offsets O_l, and
-//   prefix(entry) = O_l + (sequential partial within the block),  T_l = O_l + P_l,
-//   S' = T of the lane holding the last entry.
-// A descent picks the first lane with T_l > y and walks that lane's block alone.  Each
-// token of the run then redraws its u, repeats the MPT test and, if it fails, lands
-// in [M | S' | Q'].
-__device__ __forceinline__ void warp_max_u32(uint32_t& x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(kFull, x, o));
+// The sampler processes the flagged (doc d, word v) runs of its item in batches of 32
+// per warp (P:546 steps 4-6):
+//  phase 1 (lane per run): the lane streams the doc's packed D row with 16-byte loads
+//    (rows are 16-byte aligned) and builds S' = sum_{k in nz(D[d]), k != K1}
+//    D[d][k] What'[v][k] sequentially in ascending topic order -- the oracle's order --
+//    saving the running sum at 8 evenly spaced checkpoints in shared memory, plus
+//    C1..C3, L_d, M, the MPT threshold and Z = M + S' + Q';
+//  phase 2 (lane per token): the batch's tokens are spread over the lanes; each redraws
+//    its u, repeats the MPT test and, if it fails, lands in [M | S' | Q']: the S' descent
+//    restarts from the last checkpoint below y and walks at most one interval with the
+//    identical accumulation; the Q' descent binary-searches CP and walks one chunk.
+constexpr int kCkpt = 8;
+
+struct RunState {  // one per batch slot, shared memory
+  double Sp, M, thr, Z;
+  uint32_t j0, dbase, nnz, ck, lastk, pad;
+};
+
+#ifndef EZLDA_PF
+#define EZLDA_PF 2  // 16-byte D-row blocks in flight per lane in phase 1
+#endif
+#ifndef EZLDA_SAMP_MINB
+#define EZLDA_SAMP_MINB 4  // sampler blocks per SM the register allocation must allow
+#endif
+constexpr int kQueue = 64;  // one batch + one refill group
+
+struct __align__(16) WarpScratch {
+  double ckpt[32][kCkpt];
+  RunState st[32];
+  uint32_t q[kQueue];     // queue of flagged runs
+  uint32_t tofs[36];      // token offsets of the batch (33 used)
+};
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
 }
 
-__device__ __forceinline__ void sample_run(const Dev& d, const Buf& nxt, const WordRec& rec, const double* row,
-                                           const double* CP, uint32_t* hist, uint32_t* sbuf, uint32_t r,
-                                           uint32_t iter, RunCounters& rc) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t j0 = d.run_j0[r];
-  const uint32_t dbase = d.run_dbase[r];
-  const uint32_t len = d.run_len[r];
-  const uint32_t* Dp = d.D + dbase;
-  const uint32_t hdr = Dp[0];
+// D[d][key] by binary search in the topic-sorted row (L1-hot after phase 1)
+__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t key) {
+  uint32_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((E[mid] >> 16) < key) lo = mid + 1; else hi = mid;
+  }
+  if (lo < nnz) {
+    const uint32_t w = E[lo];
+    if ((w >> 16) == key) return w & 0xFFFFu;
+  }
+  return 0u;
+}
+
+__device__ __forceinline__ void batch_phase1(const Dev& d, const WordRec& rec, uint32_t row_s, WarpScratch& ws,
+                                             uint32_t slot, uint32_t r, uint32_t& len_out, RunCounters& rc) {
+  const uint32_t j0 = d.run_j0[r], dbase = d.run_dbase[r], len = d.run_len[r];
+  const uint32_t hdr = d.D[dbase];
   const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
-  const uint32_t* Drow = Dp + 2;
-  const uint32_t K1 = rec.K[0], K2 = rec.K[1], K3 = rec.K[2];
-  // stage (coalesced) when it fits; otherwise read the blocks straight from global memory
-  const bool staged = nnz <= (uint32_t)kDrowCap;
-  if (staged) {
-    for (uint32_t i = lane; i < nnz; i += 32) sbuf[i] = Drow[i];
-    __syncwarp();
+  const uint32_t* E = d.D + dbase + kDHdr;
+  const uint4* E4 = reinterpret_cast<const uint4*>(E);
+  const uint32_t n4 = (nnz + 3) >> 2;
+  const uint32_t ck4 = max(1u, (n4 + kCkpt - 1) / kCkpt);  // checkpoint interval in 16-byte blocks
+  double Sp = 0.0;
+  double* cp = ws.ckpt[slot];
+  uint32_t ci = 0, cc = 0;
+  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+  uint4 q = n4 ? E4[0] : z4;
+#if EZLDA_PF >= 2
+  uint4 q1 = n4 > 1 ? E4[1] : z4;
+#endif
+  for (uint32_t i = 0; i < n4; ++i) {
+#if EZLDA_PF >= 2
+    const uint4 qn = q1;
+    q1 = (i + 2 < n4) ? E4[i + 2] : z4;
+#else
+    const uint4 qn = (i + 1 < n4) ? E4[i + 1] : z4;
+#endif
+    const uint32_t rem = nnz - 4 * i;
+    // S' += D[d][k] What'[v][k], sequential in ascending topic order (row_s[K1] = 0)
+    Sp = Sp + (double)(q.x & 0xFFFFu) * lds_f64(row_s + ((q.x >> 16) << 3));
+    if (rem > 1) Sp = Sp + (double)(q.y & 0xFFFFu) * lds_f64(row_s + ((q.y >> 16) << 3));
+    if (rem > 2) Sp = Sp + (double)(q.z & 0xFFFFu) * lds_f64(row_s + ((q.z >> 16) << 3));
+    if (rem > 3) Sp = Sp + (double)(q.w & 0xFFFFu) * lds_f64(row_s + ((q.w >> 16) << 3));
+    if (++cc == ck4) {  // save the running sum after 4 ck4 entries
+      cp[ci++] = Sp;
+      cc = 0;
+    }
+    q = qn;
   }
-  const uint32_t* src = staged ? sbuf : Drow;
-  uint32_t B = (nnz + 31u) >> 5;
-  if (staged && B > 1 && !(B & 1u)) B += 1;  // odd stride: conflict-free shared-memory reads
-  const uint32_t b0 = min(lane * B, nnz), b1 = min(b0 + B, nnz);
-  double P = 0.0;
-  uint32_t c1 = 0, c2 = 0, c3 = 0, li = 0;  // li = 1 + index of the lane's last entry != K1
-  for (uint32_t i = b0; i < b1; ++i) {
-    const uint32_t e = src[i];
-    const uint32_t k = e >> 16, cnt = e & 0xFFFFu;
-    P = P + (double)cnt * row[k];  // row[K1] = 0: What'
-    c1 = (k == K1) ? cnt : c1;
-    c2 = (k == K2) ? cnt : c2;
-    c3 = (k == K3) ? cnt : c3;
-    li = (k != K1) ? i + 1 : li;
+  if (cc) cp[ci] = Sp;  // the last (partial) interval ends at S'
+  const uint32_t K1 = rec.K[0];
+  const uint32_t C1 = row_count(E, nnz, K1);
+  const uint32_t C2 = d.geff >= 2 ? row_count(E, nnz, rec.K[1]) : 0u;
+  const uint32_t C3 = d.geff >= 3 ? row_count(E, nnz, rec.K[2]) : 0u;
+  uint32_t lastk = K1;  // last topic of the row other than K1
+  if (nnz) {
+    const uint32_t kl = E[nnz - 1] >> 16;
+    lastk = (kl != K1) ? kl : (nnz >= 2 ? (E[nnz - 2] >> 16) : K1);
   }
-  const double incl = warp_incl_scan(P);
-  double O = __shfl_up_sync(kFull, incl, 1);
-  if (lane == 0) O = 0.0;
-  const double T = O + P;
-  warp_max_u32(c1);
-  warp_max_u32(c2);
-  warp_max_u32(c3);
-  warp_max_u32(li);
-  const uint32_t C1 = c1, C2 = c2, C3 = c3;
-  const uint32_t lastk = li ? (src[li - 1] >> 16) : K1;
-  const uint32_t l_last = nnz ? (nnz - 1) / B : 0;
-  const double Sp = __shfl_sync(kFull, T, l_last);
+  RunState& st = ws.st[slot];
+  st.Sp = Sp;
+  st.M = mpt_M(rec, C1, d.alpha);
+  st.thr = mpt_threshold(rec, st.M, C1, C2, C3, L, d.geff);
+  st.Z = (st.M + Sp) + rec.Qp;
+  st.j0 = j0;
+  st.dbase = dbase;
+  st.nnz = nnz;
+  st.ck = 4 * ck4;
+  st.lastk = lastk;
+  len_out = len;
   rc.runs += 1;
-  rc.words += 2 + nnz;
+  rc.words += kDHdr + nnz;
+}
 
-  const double M = mpt_M(rec, C1, d.alpha);
-  const double thr = mpt_threshold(rec, M, C1, C2, C3, L, d.geff);
-  const double MS = M + Sp;
-  const double Z = MS + rec.Qp;
-
-  // first entry (k != K1) of the S' prefix list with prefix > y; none -> last such entry
-  auto s_descent = [&](double y) -> uint32_t {
-    uint32_t m = __ballot_sync(kFull, b0 < b1 && T > y);
-    while (m) {
-      const int l = __ffs(m) - 1;
-      m &= m - 1;
-      uint32_t res = 0xFFFFFFFFu;
-      if ((int)lane == l) {
-        double s = 0.0;
-        for (uint32_t i = b0; i < b1; ++i) {
-          const uint32_t e = src[i];
-          const uint32_t k = e >> 16;
-          s = s + (double)(e & 0xFFFFu) * row[k];
-          if (k != K1 && O + s > y) {
-            res = k;
-            break;
-          }
-        }
-      }
-      res = __shfl_sync(kFull, res, l);
-      if (res != 0xFFFFFFFFu) return res;
-    }
-    return lastk;
-  };
-  // first topic k != K1 (ascending) with alpha * P(k) > y; none -> last topic != K1
-  auto q_descent = [&](double y) -> uint32_t {
-    uint32_t lo = 0, hi = d.nch;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (d.alpha * CP[mid + 1] > y) hi = mid; else lo = mid + 1;
-    }
-    for (uint32_t c = lo; c < d.nch; ++c) {
-      const uint32_t k = c * 32u + lane;
-      const double val = CP[c] + warp_incl_scan(row[k]);
-      const uint32_t m = __ballot_sync(kFull, k < d.K && k != K1 && d.alpha * val > y);
-      if (m) return c * 32u + (uint32_t)(__ffs(m) - 1);
-    }
-    return (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
-  };
-
-  for (uint32_t tb = 0; tb < len; tb += 32) {
-    const uint32_t t = tb + lane;
-    const uint32_t j = j0 + t;
-    int br = 0;  // 0: skipped by the MPT test (or no token), 1: M, 2: S', 3: Q'
-    double y = 0.0;
-    if (t < len) {
-      const double u = philox_u(d.seed, iter, d.token_base + j);
-      if (!(u < thr)) {
-        const double x = u * Z;
-        if (x < M) {
-          br = 1;
-        } else if (x < MS) {
-          br = 2;
-          y = x - M;
-        } else {
-          br = 3;
-          y = (x - M) - Sp;
-        }
+__device__ __forceinline__ void batch_token(const Dev& d, const Buf& nxt, const WordRec& rec, uint32_t row_s,
+                                            const double* CP, uint32_t* hist, const WarpScratch& ws, uint32_t i,
+                                            uint32_t iter, RunCounters& rc) {
+  uint32_t lo = 0, hi = 32;  // slot = last s with tofs[s] <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (ws.tofs[mid] <= i) lo = mid; else hi = mid;
+  }
+  const uint32_t slot = lo;
+  const RunState& st = ws.st[slot];
+  const uint32_t j = st.j0 + (i - ws.tofs[slot]);
+  const double u = philox_u(d.seed, iter, d.token_base + j);
+  if (u < st.thr) return;  // skipped by the MPT test: the doc pass already wrote K1
+  const uint32_t K1 = rec.K[0];
+  const double x = u * st.Z;
+  uint32_t topic;
+  if (x < st.M) {
+    topic = K1;  // second chance: u < M / (M + S' + Q')
+    rc.hitM += 1;
+  } else if (x < st.M + st.Sp) {
+    // S' branch: first entry (k != K1) with prefix > y; none -> last such entry.  Restart
+    // from the last checkpoint <= y and repeat phase 1's accumulation exactly.
+    const double y = x - st.M;
+    const double* cp = ws.ckpt[slot];
+    const uint32_t ncp = (st.nnz + st.ck - 1) / st.ck;
+    uint32_t c = 0;
+    while (c + 1 < ncp && !(cp[c] > y)) ++c;
+    double acc = c ? cp[c - 1] : 0.0;
+    topic = st.lastk;
+    const uint32_t* E = d.D + st.dbase + kDHdr;
+    for (uint32_t e = c * st.ck; e < st.nnz; ++e) {
+      const uint32_t w = E[e];
+      const uint32_t k = w >> 16;
+      acc = acc + (double)(w & 0xFFFFu) * lds_f64(row_s + (k << 3));
+      if (k != K1 && acc > y) {
+        topic = k;
+        break;
       }
     }
-    uint32_t topic = K1;
-    uint32_t ms = __ballot_sync(kFull, br == 2);
-    while (ms) {
-      const int l = __ffs(ms) - 1;
-      ms &= ms - 1;
-      const uint32_t tk = s_descent(__shfl_sync(kFull, y, l));
-      if ((int)lane == l) topic = tk;
+  } else {
+    // Q' branch: first topic k != K1 with alpha P(k) > y; none -> last topic != K1
+    const double y = (x - st.M) - st.Sp;
+    uint32_t a = 0, b = d.nch;
+    while (a < b) {
+      const uint32_t mid = (a + b) >> 1;
+      if (d.alpha * CP[mid + 1] > y) b = mid; else a = mid + 1;
     }
-    uint32_t mq = __ballot_sync(kFull, br == 3);
-    while (mq) {
-      const int l = __ffs(mq) - 1;
-      mq &= mq - 1;
-      const uint32_t tk = q_descent(__shfl_sync(kFull, y, l));
-      if ((int)lane == l) topic = tk;
-    }
-    if (br != 0) {
-      nxt.z[j] = (uint16_t)topic;
-      atomicAdd(&hist[topic], 1u);
-      rc.sampled += 1;
-      rc.hitM += (br == 1);
+    topic = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
+    if (a < d.nch) {
+      double acc = 0.0;
+      const uint32_t kb = a * 32u;
+      for (uint32_t q = 0; q < 32; ++q) {
+        const uint32_t k = kb + q;
+        acc = acc + lds_f64(row_s + (k << 3));
+        if (k < d.K && k != K1 && d.alpha * (CP[a] + acc) > y) {
+          topic = k;
+          break;
+        }
+      }
     }
   }
-  __syncwarp();  // sbuf is reused by the warp's next run
+  nxt.z[j] = (uint16_t)topic;
+  atomicAdd(&hist[topic], 1u);
+  rc.sampled += 1;
 }
 
 template <bool kCount>
-__global__ void __launch_bounds__(kSampWarps * 32) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter) {
+__global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* row = reinterpret_cast<double*>(smem);
   double* T = row + d.Kpad;
   double* CP = T + d.nch;
   uint32_t* hist = reinterpret_cast<uint32_t*>(CP + d.nch + 1);
+  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(
+      (reinterpret_cast<uintptr_t>(hist + d.Kpad) + 15) & ~(uintptr_t)15);  // kSampWarps entries
   __shared__ uint32_t s_cursor, s_wsum[32], s_run;
   __shared__ uint32_t s_sampled, s_hitM, s_runs, s_words;
-  __shared__ uint32_t s_drow[kSampWarps][kDrowCap];
-  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t item = blockIdx.x;
   const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
   const uint32_t ntok = d.item_ntok[item];
@@ -539,36 +628,69 @@ __global__ void __launch_bounds__(kSampWarps * 32) k_sampler(Dev d, Buf cur, Buf
     __syncthreads();
   }
   RunCounters rc{0, 0, 0, 0};
-  while (true) {
-    uint32_t grp = 0;
-    if (lane == 0) grp = atomicAdd(&s_cursor, 1u);
-    grp = __shfl_sync(kFull, grp, 0);
-    const uint32_t rb = r0 + grp * 32u;
-    if (rb >= r1) break;
-    const uint32_t r = rb + lane;
-    if (kCount) {
-      if (r < r1) {
-        const uint32_t j0 = d.run_j0[r], len = d.run_len[r];
-        for (uint32_t t = 0; t < len; ++t) atomicAdd(&hist[cur.z[j0 + t]], 1u);
-      }
-      continue;
+  if (kCount) {
+    for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) {
+      const uint32_t j0 = d.run_j0[r], len = d.run_len[r];
+      for (uint32_t t = 0; t < len; ++t) atomicAdd(&hist[cur.z[j0 + t]], 1u);
     }
-    const bool active = (r < r1) && ((d.flags[r >> 5] >> (r & 31u)) & 1u);
-    uint32_t am = __ballot_sync(kFull, active);
-    while (am) {
-      const int l = __ffs(am) - 1;
-      am &= am - 1;
-      sample_run(d, nxt, rec, row, CP, hist, s_drow[tid >> 5], rb + (uint32_t)l, iter, rc);
+  } else {
+    WarpScratch& ws = s_ws[warp];
+    const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
+    uint32_t qn = 0;
+    bool exhausted = false;
+    while (true) {
+      // refill the queue with flagged runs (warp-uniform control flow throughout)
+      while (qn < 32 && !exhausted) {
+        uint32_t grp = 0;
+        if (lane == 0) grp = atomicAdd(&s_cursor, 1u);
+        grp = __shfl_sync(kFull, grp, 0);
+        const uint32_t rb = r0 + grp * 32u;
+        if (rb >= r1) {
+          exhausted = true;
+          break;
+        }
+        const uint32_t r = rb + lane;
+        const bool act = (r < r1) && ((d.flags[r >> 5] >> (r & 31u)) & 1u);
+        const uint32_t m = __ballot_sync(kFull, act);
+        if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
+        qn += __popc(m);
+        __syncwarp();
+      }
+      if (qn == 0) break;
+      const uint32_t nb = min(qn, 32u);
+      uint32_t len = 0;
+      if (lane < nb) batch_phase1(d, rec, row_s, ws, lane, ws.q[lane], len, rc);
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      ws.tofs[lane + 1] = incl;
+      if (lane == 0) ws.tofs[0] = 0;
+      const uint32_t ntb = __shfl_sync(kFull, incl, 31);
+      __syncwarp();
+      for (uint32_t i = lane; i < ntb; i += 32) batch_token(d, nxt, rec, row_s, CP, hist, ws, i, iter, rc);
+      // drop the processed batch from the queue
+      __syncwarp();
+      {
+        const uint32_t keep = (lane + 32 < qn) ? ws.q[32 + lane] : 0u;
+        __syncwarp();
+        if (lane + 32 < qn) ws.q[lane] = keep;
+      }
+      qn -= nb;
+      __syncwarp();
     }
   }
   // per-block counters
   {
     const uint32_t smp = warp_sum(rc.sampled), hm = warp_sum(rc.hitM);
+    const uint32_t nr = warp_sum(rc.runs), nw = warp_sum(rc.words);
     if (lane == 0 && !kCount) {
       atomicAdd(&s_sampled, smp);
       atomicAdd(&s_hitM, hm);
-      atomicAdd(&s_runs, rc.runs);
-      atomicAdd(&s_words, rc.words);
+      atomicAdd(&s_runs, nr);
+      atomicAdd(&s_words, nw);
     }
   }
   __syncthreads();
@@ -621,7 +743,7 @@ __global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double
     const uint32_t dbase = d.run_dbase[r], len = d.run_len[r];
     const uint32_t hdr = d.D[dbase];
     const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
-    const uint32_t* Drow = d.D + dbase + 2;
+    const uint32_t* Drow = d.D + dbase + kDHdr;
     double carry = 0.0;
     for (uint32_t c = 0; c * 32u < nnz; ++c) {
       const uint32_t i = c * 32u + lane;
@@ -680,7 +802,9 @@ size_t word_prep_smem_bytes(uint32_t K) {
 }
 size_t sampler_smem_bytes(uint32_t K) {
   const uint32_t nch = (K + 31) / 32;
-  return word_prep_smem_bytes(K) + (size_t)nch * 32 * 4;
+  size_t b = word_prep_smem_bytes(K) + (size_t)nch * 32 * 4;
+  b = (b + 15) & ~(size_t)15;
+  return b + sizeof(WarpScratch) * kSampWarps;
 }
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
@@ -693,6 +817,11 @@ cudaError_t configure_kernels(uint32_t K) {
   if ((e = cudaFuncSetAttribute(k_sampler<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
+  if (K <= 4096) {
+    const int dh = kDocWarps * (int)(((K + 31) / 32) * 16) * 4;
+    if ((e = cudaFuncSetAttribute(k_doc_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
+    if ((e = cudaFuncSetAttribute(k_doc_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
+  }
   return cudaSuccess;
 }
 
@@ -712,7 +841,14 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
     else
       k_doc_block<false><<<n_b, 256, doc_block_smem_bytes(d.K), s>>>(d, cur, nxt, docs_b, iteration);
   }
-  if (n_w) {
+  if (n_w && d.K <= 4096) {
+    const uint32_t grid = std::min<uint32_t>((n_w + kDocWarps - 1) / kDocWarps, 148u * 16u);
+    const size_t smem = (size_t)kDocWarps * (d.Kpad / 2) * 4;
+    if (skip_test)
+      k_doc_hist<true><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
+    else
+      k_doc_hist<false><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
+  } else if (n_w) {
     const uint32_t grid = (n_w + kDocWarps - 1) / kDocWarps;
     if (skip_test)
       k_doc_warp<true><<<grid, kDocWarps * 32, 0, s>>>(d, cur, nxt, docs_w, n_w, iteration);

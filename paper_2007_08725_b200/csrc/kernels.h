@@ -6,8 +6,9 @@
 //     trid[j] u32  index of the token's run in word-major run order
 //     z[2][j] u16  topics, double-buffered (snapshot semantics)
 //     perm[j] u32  input index of token j (output order only)
-//   dofs[Dn+1] u32 token offsets of docs; D rows at dbase(d) = dofs[d] + 2d:
-//     D[dbase] = (L_d << 16) | nnz_d, D[dbase+1] = dofs[d], D[dbase+2+i] = (topic << 16) | count
+//   dofs[Dn+1] u32 token offsets of docs; D rows at ddb[d] (16-byte aligned, capacity
+//     L_d + 4 rounded up to 4 words; entries start 16-byte aligned after a 4-word header):
+//     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+4+i] = (topic << 16) | count
 //     sorted by topic (packed CSR; rebuilt every iteration)
 //   word-major runs r in [0, R) (runs of word v contiguous, docs ascending):
 //     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
@@ -24,6 +25,8 @@
 
 namespace ezl {
 
+constexpr uint32_t kDHdr = 4;  // header words in front of every packed D row
+
 struct Counters {  // device-side per-iteration counters
   unsigned long long skip_S, skip_M, sampled, active_runs, drow_words, d_nnz;
 };
@@ -35,6 +38,7 @@ struct Dev {
   uint64_t seed, token_base;
   // static structure
   const uint32_t* dofs;
+  const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 4 words)
   const uint32_t* tw;
   const uint32_t* trid;
   const uint32_t* run_j0;

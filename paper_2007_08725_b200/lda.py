@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libezlda.so")
+LIB_PATH = os.environ.get("EZLDA_LIB") or os.path.join(HERE, "libezlda.so")
 
 EZLDA_W_HYBRID, EZLDA_W_ALL_DENSE, EZLDA_W_ALL_SPARSE = 0, 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_RANGE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_NCCL", 6: "E_STATE"}
