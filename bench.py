@@ -159,8 +159,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=1_000_000, help="oracle sample size for cpu_baseline")
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--ref-tokens", type=int, default=150_000, help="oracle sample size per --impl reference step")
+    ap.add_argument("--doc-block-kb", type=int, default=0, help="sampler L2 tiling (KiB of D rows per block; 0 = off)")
     ap.add_argument("--ncu-traffic", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
-    ap.add_argument("--curve", action="store_true", help="also print the per-iteration curve to stderr")
     args = ap.parse_args()
 
     rank = env_int("RANK", 0)
@@ -208,7 +208,8 @@ def main():
     torch.cuda.set_stream(stream)
     t_create = time.perf_counter()
     ez = lda.EzLDA(w, d, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
-                   nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream)
+                   nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream,
+                   doc_block_kb=args.doc_block_kb)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t_create
 
@@ -300,7 +301,8 @@ def main():
             dist.barrier()
         te = time.perf_counter()
         ez2 = lda.EzLDA(hw, hd, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
-                        nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream)
+                        nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream,
+                   doc_block_kb=args.doc_block_kb)
         ez2.iterate(args.warmup + args.steps)
         ez2.topics(out=hz)
         torch.cuda.synchronize()

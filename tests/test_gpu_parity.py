@@ -187,7 +187,8 @@ def test_appendix_a_state_loglik(ez):
 
 @pytest.mark.parametrize("knobs", [
     dict(w_mode=1), dict(w_mode=2), dict(dense_threshold=3), dict(split_threshold=64),
-    dict(split_threshold=64, w_mode=1), dict(g=1), dict(g=3),
+    dict(split_threshold=64, w_mode=1), dict(g=1), dict(g=3), dict(doc_block_kb=1),
+    dict(doc_block_kb=1, split_threshold=100),
 ])
 def test_knob_invariance(ez, tiny, knobs):
     """Dense threshold, W mode, region split and g change speed only: T bit-identical."""
