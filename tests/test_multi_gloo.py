@@ -1,0 +1,83 @@
+"""World-size-2 host-side test of the doc-partitioned multi-GPU protocol on CPU (gloo).
+
+Each rank owns a contiguous, token-balanced document range (lda.partition_docs, the
+partition of P:1137-1140) with its global token base; every iteration the ranks sum their
+local W counts (the per-iteration merge of P:1145, NCCL all-reduce on the GPUs, gloo here)
+and sample against the merged snapshot.  The concatenated topics must equal the
+single-process chain bit for bit.  The per-rank compute is the CPU oracle (test harness),
+so this exercises the partition, token bases and the exchange protocol, not the kernels.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2007_08725_b200.lda import partition_docs
+from paper_2007_08725_b200.synth import SAMPLER_SEED, planted_corpus_np
+
+N_DOCS, V, K, ITERS = 120, 400, 12, 4
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+
+    w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
+    L = np.bincount(d, minlength=N_DOCS)
+    bounds = partition_docs(L, world)
+    cum = np.concatenate([[0], np.cumsum(L)])
+    t0, t1 = int(cum[bounds[rank]]), int(cum[bounds[rank + 1]])
+    shard = oracle.OracleLDA(w[t0:t1], d[t0:t1] - bounds[rank], bounds[rank + 1] - bounds[rank], V, K,
+                             seed=SAMPLER_SEED, token_base=t0)
+    for _ in range(ITERS):
+        Wl = torch.from_numpy(shard.counts()[1].astype(np.int64))
+        dist.all_reduce(Wl, op=dist.ReduceOp.SUM)  # the per-iteration W merge
+        Wg = Wl.numpy().astype(np.int32)
+        shard.iterate(1, Wg, Wg.sum(0).astype(np.int32))
+    z = torch.from_numpy(shard.topics().astype(np.int64))
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([len(z)]))
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.full((mx,), -1, dtype=torch.int64)
+    pad[: len(z)] = z
+    parts = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    if rank == 0:
+        allz = np.concatenate([p[: int(s.item())].numpy() for p, s in zip(parts, sizes)])
+        np.save(out, allz)
+    dist.destroy_process_group()
+
+
+def test_partition_docs_balanced():
+    L = np.random.default_rng(0).integers(1, 500, size=1000)
+    for P in (1, 2, 3, 8):
+        b = partition_docs(L, P)
+        assert b[0] == 0 and b[-1] == len(L) and all(x <= y for x, y in zip(b, b[1:]))
+        tok = [L[b[i]:b[i + 1]].sum() for i in range(P)]
+        assert max(tok) - min(tok) <= 2 * L.max()
+
+
+def test_two_rank_gloo_equals_single(tmp_path):
+    from oracle import oracle
+
+    oracle.build()
+    out = str(tmp_path / "z.npy")
+    mp.spawn(worker, args=(2, free_port(), out), nprocs=2, join=True)
+    w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
+    ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED)
+    ref.iterate(ITERS)
+    assert np.array_equal(np.load(out), ref.topics().astype(np.int64))
