@@ -75,8 +75,9 @@ typedef struct {
   void* stream;              /* cudaStream_t to run on, or NULL (library creates one)      */
   uint32_t input_on_device;  /* 1: word_ids/doc_ids passed to ezlda_create are device ptrs */
   uint32_t no_phase_timing;  /* 1: do not record per-phase CUDA events                     */
-  uint32_t doc_block_kb;     /* L2 tiling: cut dense-word sampler items at doc blocks of    */
-                             /* this many KiB of D rows, run them block-major; 0 -> off     */
+  uint32_t doc_block_kb;     /* L2 tiling: cut hot-word sampler items at doc windows of     */
+                             /* this many KiB of D rows, run them window-major;            */
+                             /* 0 -> 32768 (32 MiB); 0xFFFFFFFF -> one window (off)        */
 } ezlda_options;
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL

@@ -148,12 +148,12 @@ __global__ void k_wrun(const uint32_t* vs, uint32_t R, uint32_t V, uint32_t* wru
   }
 }
 
-// item heads: first run of each word, and dense-word region boundaries every `split` tokens
 // item heads: first run of each word; for dense words also region boundaries every `split`
-// tokens and doc-block boundaries (run_dbase / blk_words changes)
+// tokens and, for hot words (>= cut_min tokens), doc-window boundaries
+// (run_dbase / blk_words changes)
 __global__ void k_item_heads(const uint32_t* vs, const uint32_t* wrun, const uint32_t* tokpre,
                              const uint32_t* run_dbase, uint32_t R, uint32_t Vd, uint32_t split, uint32_t blk_words,
-                             uint32_t* head) {
+                             uint32_t cut_min, uint32_t* head) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < R) {
     const uint32_t v = vs[r];
@@ -162,7 +162,7 @@ __global__ void k_item_heads(const uint32_t* vs, const uint32_t* wrun, const uin
     if (!h && v < Vd) {
       const uint32_t b = tokpre[first];
       h = ((tokpre[r] - b) / split) != ((tokpre[r - 1] - b) / split);
-      h |= (run_dbase[r] / blk_words) != (run_dbase[r - 1] / blk_words);
+      if (tokpre[wrun[v + 1]] - b >= cut_min) h |= (run_dbase[r] / blk_words) != (run_dbase[r - 1] / blk_words);
     }
     head[r] = h;
   }
@@ -213,6 +213,7 @@ struct ezlda {
   uint32_t n_items = 0, n_docs_w = 0, n_docs_b = 0;
   uint64_t tail_cap = 0;
   uint64_t Dwords = 0;
+  uint32_t cut_min = 0;
   double alpha = 0, beta = 0;
   uint64_t seed = 0;
   uint32_t g = 2;
@@ -322,6 +323,8 @@ void fill_dev(ezlda* h) {
   d.nch = (h->K + 31) / 32;
   d.Kpad = d.nch * 32;
   d.Vd = h->Vd;
+  d.rs = ezl::wrow_stride(h->K);
+  d.segw = ezl::seg_width(h->K);
   d.geff = std::min<uint32_t>(h->g, h->K - 1);
   d.alpha = h->alpha;
   d.beta = h->beta;
@@ -391,12 +394,13 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     if (L[d] > 65535) return h->fail(EZLDA_E_RANGE, "doc %u has %u tokens (> 65535, P:753)", d, L[d]);
   std::vector<uint32_t> dofs(h->Dn + 1, 0);
   for (uint32_t d = 0; d < h->Dn; ++d) dofs[d + 1] = dofs[d] + L[d];
-  // D rows: 2 header words + L_d entries, padded to 16 bytes (TMA bulk-copy granularity)
+  // D rows: an 8-word header + min(L_d, K) entries padded to a multiple of 8 (one 32-byte
+  // sector per 8 entries; rows start sector aligned)
   std::vector<uint32_t> ddb(h->Dn);
   uint64_t dwords = 0;
   for (uint32_t d = 0; d < h->Dn; ++d) {
     ddb[d] = (uint32_t)dwords;
-    dwords += ((uint64_t)L[d] + ezl::kDHdr + 3) & ~3ull;
+    dwords += ezl::kDHdr + ((std::min<uint64_t>(L[d], h->K) + 7) & ~7ull);
   }
   if (dwords >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "D storage >= 2^32 words per shard");
   h->Dwords = dwords;
@@ -538,11 +542,17 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(len32);
   const uint32_t split = o.split_threshold ? o.split_threshold : 10000u;
   EZ_ALLOC(h, ihead, uint32_t, R);
-  // doc blocks of doc_block_kb KiB of D rows (0 = off): dense-word items are cut at block
-  // boundaries and run block-major, so the D rows in use at any time share the L2
-  const uint64_t blk_kb = o.doc_block_kb ? o.doc_block_kb : 0xFFFFFFFFull;
+  // L2 doc windows of doc_block_kb KiB of D rows (0 = 32 MiB): the items of hot words (at
+  // least 256 tokens per window on average) are cut at window boundaries and run
+  // window-major, heavy first -- every D row of the window is then read by many items
+  // while it is L2 resident; the other words' items (too few runs per window to amortise
+  // the staged What' row) run uncut after them
+  const uint64_t blk_kb = o.doc_block_kb ? o.doc_block_kb : 32768ull;
   const uint32_t blk_words = (uint32_t)std::min<uint64_t>(blk_kb * 256ull, 0xFFFFFFFFull);
-  k_item_heads<<<blocks(R), 256, 0, s>>>(vs, wrun, tokpre, run_dbase, R, h->Vd, split, blk_words, ihead);
+  const uint64_t nwin = (h->Dwords + blk_words - 1) / blk_words;
+  const uint32_t cut_min = (uint32_t)std::min<uint64_t>(256ull * nwin, 0xFFFFFFFFull);
+  h->cut_min = cut_min;
+  k_item_heads<<<blocks(R), 256, 0, s>>>(vs, wrun, tokpre, run_dbase, R, h->Vd, split, blk_words, cut_min, ihead);
   EZ_ALLOC(h, r_iota, uint32_t, R);
   EZ_ALLOC(h, r0s, uint32_t, R);
   EZ_ALLOC(h, d_ni, uint32_t, 1);
@@ -568,15 +578,15 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(vs);
   h->release(tokpre);
   h->release(wrun);
-  // order: doc-block-major for dense-word items (tail words, whose single item spans all docs,
-  // last), heavy first within a block; the hardware block scheduler then balances the tail
-  //
+  // order: hot-word items window-major, heavy first within a window; then the other items
+  // heavy first; the hardware block scheduler balances the tail
   std::vector<uint32_t> order(NI);
   std::iota(order.begin(), order.end(), 0u);
   auto key = [&](uint32_t a) {
-    const uint64_t tail = it5[5 * a] >= h->Vd ? 1u : 0u;
-    const uint64_t blk = tail ? 0u : it5[5 * a + 4];
-    return (tail << 63) | (blk << 32) | (uint64_t)(0xFFFFFFFFu - it5[5 * a + 3]);
+    const uint32_t v = it5[5 * a];
+    const uint64_t cold = (v >= h->Vd || cnt_local[h->origword[v]] < cut_min) ? 1u : 0u;
+    const uint64_t blk = cold ? 0u : it5[5 * a + 4];
+    return (cold << 63) | (blk << 32) | (uint64_t)(0xFFFFFFFFu - it5[5 * a + 3]);
   };
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
   std::vector<uint32_t> iw(NI), ir0(NI), ir1(NI), int_(NI);
@@ -631,6 +641,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
+  EZ_ALLOC(h, d.wrow, double, (size_t)h->Vd * d.rs);
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
   EZ_ALLOC(h, d.ctr, ezl::Counters, 1);

@@ -84,6 +84,20 @@ __device__ void chunk_prefix(const double* row, uint32_t nch, double* T, double*
   __syncthreads();
 }
 
+// Q' prefix table of a staged What' row: QP[k] = alpha * P(k) with P(k) as above (the
+// chunk prefix CP[k/32] plus the sequential sum inside the chunk).  QP is non-decreasing
+// and QP[Kpad-1] = alpha CP[nch] = Q'; the Q' descent becomes one binary search.
+__device__ void q_prefix(const double* row, uint32_t nch, const double* CP, double alpha, double* QP) {
+  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
+    double acc = 0.0;
+    for (uint32_t t = 0; t < 32; ++t) {
+      acc = acc + row[c * 32 + t];
+      QP[c * 32 + t] = alpha * (CP[c] + acc);
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------------------------
 // top-4 (value desc, topic asc) -- P:546 step 1, ties to the smaller topic.
 // ---------------------------------------------------------------------------------
@@ -208,6 +222,11 @@ __global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
   __syncthreads();
   chunk_prefix(row, d.nch, T, CP);
   if (tid == 0) d.rec[v].Qp = d.alpha * CP[d.nch];
+  if (v < d.Vd) {  // What'[v] | QP for the sampler's bulk copy (dense words)
+    double* out = d.wrow + (size_t)v * d.rs;
+    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) out[k] = row[k];
+    q_prefix(row, d.nch, CP, d.alpha, out + d.Kpad);
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -242,6 +261,7 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
       nxt.z[j] = r.K[0];
       ++n_skip;
     } else {
+      nxt.z[j] = kUnsampled;  // the sampler draws it
       const uint32_t rid = d.trid[j];
       atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
     }
@@ -289,6 +309,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf
       if (x) hist[w] = 0;
       nnz += __popc(mlo) + __popc(mhi);
     }
+    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[kDHdr + p] = 0u;  // pad to 8
     if (lane == 0) {
       Drow[0] = (L << 16) | nnz;
       Drow[1] = j0;
@@ -361,6 +382,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf
     ucnt[p] = (uint16_t)cnt;
     Drow[kDHdr + p] = ((uint32_t)ukey[p] << 16) | cnt;
   }
+  for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[kDHdr + p] = 0u;  // pad to 8
   if (lane == 0) {
     Drow[0] = (L << 16) | nnz;
     Drow[1] = j0;
@@ -398,6 +420,7 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
   __syncthreads();
   uint32_t* Drow = d.D + dbase;
   const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run);
+  for (uint32_t p = nnz + tid; p < ((nnz + 7u) & ~7u); p += nt) Drow[kDHdr + p] = 0u;  // pad to 8
   if (tid == 0) {
     Drow[0] = (L << 16) | nnz;
     Drow[1] = j0;
@@ -416,42 +439,54 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
 // ---------------------------------------------------------------------------------
 // H5+H6: the residual three-branch sampler + W/n_k rebuild (one block per item).
 // ---------------------------------------------------------------------------------
+//
+// A block owns one work item (word v, a range of its (doc, word) runs).  What'[v] (Eq 6,
+// the K1 entry zeroed) and its chunk prefix CP are staged in shared memory: dense words
+// with ONE TMA bulk copy (cp.async.bulk + mbarrier) of the row word-prep wrote, tail words
+// from beta / den_k plus the word's packed nonzeros.  Warps take groups of 32 runs from an
+// in-block cursor, queue the flagged ones (a token of the run failed the doc pass's MPT
+// test) and process them in batches (P:546 steps 4-6):
+//
+//  A (lane per run)      run table + D-row header; the row is cut into segments of segw
+//                        entries (8 = one 32-byte sector); a batch admits runs while the
+//                        segment total fits kSegCap;
+//  B (lane per segment)  all 32 lanes busy; consecutive lanes read consecutive sectors of
+//                        a row (coalesced): partial[s] = sequential sum over the segment
+//                        of D[d][k] What'[v][k] in ascending topic order; C1..C3 =
+//                        D[d][K1..K3] are picked up by the lane whose segment holds K_j;
+//  C (lane per run)      P[s] = P[s-1] + partial[s] sequentially over the run's segments,
+//                        S' = P[last]; M (Eq 8), the MPT threshold (Eq 10), Z = M + S' + Q';
+//  D (lane per token)    u (Philox), MPT retest (the doc pass already wrote K1 for skipped
+//                        tokens), x = u Z lands in [M | S' | Q']; S' descent: the first
+//                        segment with P[s] > y (binary search), then the walk
+//                        P[s-1] + (sequential sum inside the segment) -- the same prefix
+//                        definition, so the walk ends exactly at P[s]; Q' descent: binary
+//                        search over CP, then one 32-topic chunk.
+// The S' prefix is a two-level (segment, entry) sum, like the Q' prefix: it differs from
+// the oracle's single sequential sum by rounding only.
 struct RunCounters {
   uint32_t sampled, hitM, runs, words;
 };
 
-// The sampler processes the flagged (doc d, word v) runs of its item in batches of 32
-// per warp (P:546 steps 4-6):
-//  phase 1 (lane per run): the lane streams the doc's packed D row with 16-byte loads
-//    (rows are 16-byte aligned) and builds S' = sum_{k in nz(D[d]), k != K1}
-//    D[d][k] What'[v][k] sequentially in ascending topic order -- the oracle's order --
-//    saving the running sum at 8 evenly spaced checkpoints in shared memory, plus
-//    C1..C3, L_d, M, the MPT threshold and Z = M + S' + Q';
-//  phase 2 (lane per token): the batch's tokens are spread over the lanes; each redraws
-//    its u, repeats the MPT test and, if it fails, lands in [M | S' | Q']: the S' descent
-//    restarts from the last checkpoint below y and walks at most one interval with the
-//    identical accumulation; the Q' descent binary-searches CP and walks one chunk.
-constexpr int kCkpt = 8;
-
-struct RunState {  // one per batch slot, shared memory
-  double Sp, M, thr, Z;
-  uint32_t j0, dbase, nnz, ck, lastk, pad;
-};
-
-#ifndef EZLDA_PF
-#define EZLDA_PF 2  // 16-byte D-row blocks in flight per lane in phase 1
-#endif
-#ifndef EZLDA_SAMP_MINB
-#define EZLDA_SAMP_MINB 4  // sampler blocks per SM the register allocation must allow
-#endif
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct __align__(16) WarpScratch {
-  double ckpt[32][kCkpt];
-  RunState st[32];
-  uint32_t q[kQueue];     // queue of flagged runs
-  uint32_t tofs[36];      // token offsets of the batch (33 used)
+struct RunState {  // one per batch slot, shared memory
+  double Sp, M, Z;
+  uint32_t j0, ebase, nnz, soff, nseg, tofs, lastk, C1;
 };
+
+struct __align__(16) WarpScratch {
+  double P[kSegCap];  // segment prefixes of the batch, flattened
+  RunState st[32];
+  uint32_t q[kQueue];  // queue of flagged runs
+};
+
+// 32-byte (one sector) read-only load
+__device__ __forceinline__ void ldg256(const uint32_t* p, uint4& a, uint4& b) {
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
 
 __device__ __forceinline__ double lds_f64(uint32_t addr) {
   double v;
@@ -459,181 +494,303 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
-// D[d][key] by binary search in the topic-sorted row (L1-hot after phase 1)
-__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t key) {
-  uint32_t lo = 0, hi = nnz;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if ((E[mid] >> 16) < key) lo = mid + 1; else hi = mid;
-  }
-  if (lo < nnz) {
-    const uint32_t w = E[lo];
-    if ((w >> 16) == key) return w & 0xFFFFu;
-  }
-  return 0u;
+// D[d][k] What'[v][k] of one packed entry (topic << 16 | count); padding (0) adds +0.0
+__device__ __forceinline__ double entry_term(uint32_t w, uint32_t row_s) {
+  return (double)(w & 0xFFFFu) * lds_f64(row_s + ((w >> 16) << 3));
 }
 
-__device__ __forceinline__ void batch_phase1(const Dev& d, const WordRec& rec, uint32_t row_s, WarpScratch& ws,
-                                             uint32_t slot, uint32_t r, uint32_t& len_out, RunCounters& rc) {
-  const uint32_t j0 = d.run_j0[r], dbase = d.run_dbase[r], len = d.run_len[r];
-  const uint32_t hdr = d.D[dbase];
-  const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
-  const uint32_t* E = d.D + dbase + kDHdr;
-  const uint4* E4 = reinterpret_cast<const uint4*>(E);
-  const uint32_t n4 = (nnz + 3) >> 2;
-  const uint32_t ck4 = max(1u, (n4 + kCkpt - 1) / kCkpt);  // checkpoint interval in 16-byte blocks
-  double Sp = 0.0;
-  double* cp = ws.ckpt[slot];
-  uint32_t ci = 0, cc = 0;
-  const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-  uint4 q = n4 ? E4[0] : z4;
-#if EZLDA_PF >= 2
-  uint4 q1 = n4 > 1 ? E4[1] : z4;
-#endif
-  for (uint32_t i = 0; i < n4; ++i) {
-#if EZLDA_PF >= 2
-    const uint4 qn = q1;
-    q1 = (i + 2 < n4) ? E4[i + 2] : z4;
-#else
-    const uint4 qn = (i + 1 < n4) ? E4[i + 1] : z4;
-#endif
-    const uint32_t rem = nnz - 4 * i;
-    // S' += D[d][k] What'[v][k], sequential in ascending topic order (row_s[K1] = 0)
-    Sp = Sp + (double)(q.x & 0xFFFFu) * lds_f64(row_s + ((q.x >> 16) << 3));
-    if (rem > 1) Sp = Sp + (double)(q.y & 0xFFFFu) * lds_f64(row_s + ((q.y >> 16) << 3));
-    if (rem > 2) Sp = Sp + (double)(q.z & 0xFFFFu) * lds_f64(row_s + ((q.z >> 16) << 3));
-    if (rem > 3) Sp = Sp + (double)(q.w & 0xFFFFu) * lds_f64(row_s + ((q.w >> 16) << 3));
-    if (++cc == ck4) {  // save the running sum after 4 ck4 entries
-      cp[ci++] = Sp;
-      cc = 0;
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
+               "l"(src), "r"(bytes), "r"(mbar_s)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar_s, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(mbar_s), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// One batch of flagged runs (warp-uniform control flow).  Returns the number of queue
+// entries consumed.  kSeg8: segw == 8 (one sector per segment; K <= 8 kSegCap).
+template <bool kSeg8>
+__device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, const WordRec& rec, uint32_t row_s,
+                                                 const double* QP, uint32_t* hist, WarpScratch& ws, uint32_t qn,
+                                                 uint32_t iter, RunCounters& rc) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t segw = kSeg8 ? 8u : d.segw;
+  const uint32_t K1 = rec.K[0];
+  // ---- A: run table + header, segment admission
+  const uint32_t nc = min(qn, 32u);
+  uint32_t j0 = 0, dbase = 0, len = 0, hdr = 0, nseg = 0;
+  if (lane < nc) {
+    const uint32_t r = ws.q[lane];
+    j0 = d.run_j0[r];
+    dbase = d.run_dbase[r];
+    len = d.run_len[r];
+    hdr = d.D[dbase];
+    nseg = ((hdr & 0xFFFFu) + segw - 1u) / segw;
+  }
+  uint32_t sincl = nseg, tincl;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, sincl, o);
+    if (lane >= (uint32_t)o) sincl += y;
+  }
+  const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kSegCap));  // >= 1
+  const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
+  const uint32_t soff = sincl - nseg;
+  tincl = (lane < nb) ? len : 0u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, tincl, o);
+    if (lane >= (uint32_t)o) tincl += y;
+  }
+  const uint32_t ntb = __shfl_sync(kFull, tincl, 31);
+  const uint32_t tofs = tincl - ((lane < nb) ? len : 0u);
+  if (lane < nb) {
+    RunState& st = ws.st[lane];
+    st.j0 = j0;
+    st.ebase = dbase + kDHdr;
+    st.nnz = hdr & 0xFFFFu;
+    st.soff = soff;
+    st.nseg = nseg;
+    st.tofs = tofs;
+    st.C1 = 0u;
+  }
+  __syncwarp();
+  // slot of the item with index B0 + lane, items numbered by run: first = per-run start
+  // offsets held by the run lanes (soff / tofs), ascending
+  auto slot_of = [&](uint32_t B0, uint32_t first) -> uint32_t {
+    const bool inw = lane < nb && first >= B0 && first < B0 + 32u;
+    const uint32_t bits = __reduce_or_sync(kFull, inw ? (1u << (first - B0)) : 0u);
+    const uint32_t nbefore = __popc(__ballot_sync(kFull, lane < nb && first < B0));
+    return nbefore + __popc(bits & (0xFFFFFFFFu >> (31u - lane))) - 1u;
+  };
+  // ---- B: lane per segment (one 32-byte sector = 8 entries per load); the next round's
+  //      sector is loaded before this round's terms are computed
+  uint32_t slot_c = 0, e0_c = 0;
+  uint4 qa_c = make_uint4(0u, 0u, 0u, 0u), qb_c = qa_c;
+  const uint32_t* p_c = nullptr;
+  auto locate = [&](uint32_t B0, uint32_t& slot, uint32_t& e0) -> const uint32_t* {
+    slot = slot_of(B0, soff);
+    const RunState& st = ws.st[slot];
+    e0 = (B0 + lane - st.soff) * segw;
+    return d.D + st.ebase + e0;
+  };
+  if (T) {
+    p_c = locate(0, slot_c, e0_c);
+    if (lane < T) ldg256(p_c, qa_c, qb_c);
+  }
+  for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
+    uint32_t slot_n = 0, e0_n = 0;
+    uint4 qa_n = make_uint4(0u, 0u, 0u, 0u), qb_n = qa_n;
+    const uint32_t* p_n = nullptr;
+    if (B0 + 32u < T) {
+      p_n = locate(B0 + 32u, slot_n, e0_n);
+      if (B0 + 32u + lane < T) ldg256(p_n, qa_n, qb_n);
     }
-    q = qn;
+    if (B0 + lane < T) {
+      const uint32_t nnz = ws.st[slot_c].nnz;
+      double acc = 0.0;
+      for (uint32_t b = 0; kSeg8 || (b < segw && e0_c + b < nnz); b += 8u) {
+        if (b) ldg256(p_c + b, qa_c, qb_c);
+        acc = acc + entry_term(qa_c.x, row_s);
+        acc = acc + entry_term(qa_c.y, row_s);
+        acc = acc + entry_term(qa_c.z, row_s);
+        acc = acc + entry_term(qa_c.w, row_s);
+        acc = acc + entry_term(qb_c.x, row_s);
+        acc = acc + entry_term(qb_c.y, row_s);
+        acc = acc + entry_term(qb_c.z, row_s);
+        acc = acc + entry_term(qb_c.w, row_s);
+        // C1 = D[d][K1] (Eq 8): found by the lane whose sorted topics bracket K1
+        const uint32_t hi = (e0_c + b + 8u <= nnz) ? (qb_c.w >> 16) : 0xFFFFu;
+        if ((qa_c.x >> 16) <= K1 && K1 <= hi) {
+          const uint32_t w[8] = {qa_c.x, qa_c.y, qa_c.z, qa_c.w, qb_c.x, qb_c.y, qb_c.z, qb_c.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if ((w[i] >> 16) == K1 && (w[i] & 0xFFFFu)) ws.st[slot_c].C1 = w[i] & 0xFFFFu;
+        }
+        if (kSeg8) break;
+      }
+      ws.P[B0 + lane] = acc;
+    }
+    slot_c = slot_n;
+    e0_c = e0_n;
+    p_c = p_n;
+    qa_c = qa_n;
+    qb_c = qb_n;
   }
-  if (cc) cp[ci] = Sp;  // the last (partial) interval ends at S'
-  const uint32_t K1 = rec.K[0];
-  const uint32_t C1 = row_count(E, nnz, K1);
-  const uint32_t C2 = d.geff >= 2 ? row_count(E, nnz, rec.K[1]) : 0u;
-  const uint32_t C3 = d.geff >= 3 ? row_count(E, nnz, rec.K[2]) : 0u;
-  uint32_t lastk = K1;  // last topic of the row other than K1
-  if (nnz) {
-    const uint32_t kl = E[nnz - 1] >> 16;
-    lastk = (kl != K1) ? kl : (nnz >= 2 ? (E[nnz - 2] >> 16) : K1);
+  __syncwarp();
+  // ---- C: lane per run
+  if (lane < nb) {
+    RunState& st = ws.st[lane];
+    double acc = 0.0;
+    for (uint32_t s = soff; s < soff + nseg; ++s) {
+      acc = acc + ws.P[s];
+      ws.P[s] = acc;
+    }
+    const uint32_t nnz = st.nnz;
+    const uint32_t* E = d.D + st.ebase;
+    uint32_t lastk = K1;  // last topic of the row other than K1
+    if (nnz) {
+      const uint32_t kl = __ldg(E + nnz - 1) >> 16;
+      lastk = (kl != K1) ? kl : (nnz >= 2 ? (__ldg(E + nnz - 2) >> 16) : K1);
+    }
+    st.Sp = acc;
+    st.M = mpt_M(rec, st.C1, d.alpha);
+    st.Z = (st.M + acc) + rec.Qp;
+    st.lastk = lastk;
+    rc.runs += 1;
+    rc.words += 1u + nnz;
   }
-  RunState& st = ws.st[slot];
-  st.Sp = Sp;
-  st.M = mpt_M(rec, C1, d.alpha);
-  st.thr = mpt_threshold(rec, st.M, C1, C2, C3, L, d.geff);
-  st.Z = (st.M + Sp) + rec.Qp;
-  st.j0 = j0;
-  st.dbase = dbase;
-  st.nnz = nnz;
-  st.ck = 4 * ck4;
-  st.lastk = lastk;
-  len_out = len;
-  rc.runs += 1;
-  rc.words += kDHdr + nnz;
+  __syncwarp();
+  // ---- D: lane per token; the doc pass left kUnsampled in z^i for the tokens that failed
+  //      the MPT test (the others already hold K1)
+  for (uint32_t B0 = 0; B0 < ntb; B0 += 32u) {
+    const uint32_t slot = slot_of(B0, tofs);
+    const uint32_t i = B0 + lane;
+    if (i >= ntb) continue;
+    const RunState& st = ws.st[slot];
+    const uint32_t j = st.j0 + (i - st.tofs);
+    if (nxt.z[j] != kUnsampled) continue;  // skipped by the MPT test
+    const double u = philox_u(d.seed, iter, d.token_base + j);
+    const double x = u * st.Z;
+    uint32_t topic;
+    if (x < st.M) {
+      topic = K1;  // second chance: u < M / (M + S' + Q')
+      rc.hitM += 1;
+    } else if (x < st.M + st.Sp) {
+      // S' branch: first segment with P > y, then the walk inside it
+      const double y = x - st.M;
+      uint32_t a = st.soff, b = st.soff + st.nseg - 1u;
+      while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (ws.P[mid] > y) b = mid; else a = mid + 1u;
+      }
+      const double base = (a > st.soff) ? ws.P[a - 1u] : 0.0;
+      const uint32_t e0 = (a - st.soff) * segw;
+      const uint32_t e1 = min(e0 + segw, st.nnz);
+      const uint32_t* E = d.D + st.ebase;
+      double acc = 0.0;
+      uint32_t last = 0xFFFFFFFFu;
+      topic = 0xFFFFFFFFu;
+      for (uint32_t e = e0; e < e1; ++e) {
+        const uint32_t w = __ldg(E + e);
+        const uint32_t k = w >> 16;
+        acc = acc + entry_term(w, row_s);
+        if (k != K1) {
+          last = k;
+          if (base + acc > y) {
+            topic = k;
+            break;
+          }
+        }
+      }
+      if (topic == 0xFFFFFFFFu) topic = (last != 0xFFFFFFFFu) ? last : st.lastk;  // rounding at S' end
+    } else {
+      // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
+      // is flat across K1); none -> last topic != K1
+      const double y = (x - st.M) - st.Sp;
+      uint32_t a = 0, b = d.Kpad - 1u;
+      while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (QP[mid] > y) b = mid; else a = mid + 1u;
+      }
+      if (a == K1 && QP[a] > y) ++a;  // only when K1 = 0 and y < 0
+      if (a >= d.K || !(QP[a] > y)) a = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
+      topic = a;
+    }
+    nxt.z[j] = (uint16_t)topic;
+    atomicAdd(&hist[topic], 1u);
+    rc.sampled += 1;
+  }
+  __syncwarp();
+  return nb;
 }
 
-__device__ __forceinline__ void batch_token(const Dev& d, const Buf& nxt, const WordRec& rec, uint32_t row_s,
-                                            const double* CP, uint32_t* hist, const WarpScratch& ws, uint32_t i,
-                                            uint32_t iter, RunCounters& rc) {
-  uint32_t lo = 0, hi = 32;  // slot = last s with tofs[s] <= i
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (ws.tofs[mid] <= i) lo = mid; else hi = mid;
-  }
-  const uint32_t slot = lo;
-  const RunState& st = ws.st[slot];
-  const uint32_t j = st.j0 + (i - ws.tofs[slot]);
-  const double u = philox_u(d.seed, iter, d.token_base + j);
-  if (u < st.thr) return;  // skipped by the MPT test: the doc pass already wrote K1
-  const uint32_t K1 = rec.K[0];
-  const double x = u * st.Z;
-  uint32_t topic;
-  if (x < st.M) {
-    topic = K1;  // second chance: u < M / (M + S' + Q')
-    rc.hitM += 1;
-  } else if (x < st.M + st.Sp) {
-    // S' branch: first entry (k != K1) with prefix > y; none -> last such entry.  Restart
-    // from the last checkpoint <= y and repeat phase 1's accumulation exactly.
-    const double y = x - st.M;
-    const double* cp = ws.ckpt[slot];
-    const uint32_t ncp = (st.nnz + st.ck - 1) / st.ck;
-    uint32_t c = 0;
-    while (c + 1 < ncp && !(cp[c] > y)) ++c;
-    double acc = c ? cp[c - 1] : 0.0;
-    topic = st.lastk;
-    const uint32_t* E = d.D + st.dbase + kDHdr;
-    for (uint32_t e = c * st.ck; e < st.nnz; ++e) {
-      const uint32_t w = E[e];
-      const uint32_t k = w >> 16;
-      acc = acc + (double)(w & 0xFFFFu) * lds_f64(row_s + (k << 3));
-      if (k != K1 && acc > y) {
-        topic = k;
-        break;
+// W / n_k of one item from its topic histogram (dense rows: atomics, the item may be one
+// of several regions of the word; tail rows: ordered compaction into the packed row).
+__device__ void item_epilogue(const Dev& d, const Buf& nxt, uint32_t v, const uint32_t* hist, uint32_t* s_wsum,
+                              uint32_t* s_run) {
+  const uint32_t tid = threadIdx.x;
+  if (v < d.Vd) {
+    int32_t* Wrow = nxt.Wd + (size_t)v * d.K;
+    for (uint32_t k = tid; k < d.K; k += blockDim.x) {
+      const uint32_t c = hist[k];
+      if (c) {
+        atomicAdd(&Wrow[k], (int32_t)c);
+        atomicAdd(&nxt.nk[k], (int32_t)c);
       }
     }
   } else {
-    // Q' branch: first topic k != K1 with alpha P(k) > y; none -> last topic != K1
-    const double y = (x - st.M) - st.Sp;
-    uint32_t a = 0, b = d.nch;
-    while (a < b) {
-      const uint32_t mid = (a + b) >> 1;
-      if (d.alpha * CP[mid + 1] > y) b = mid; else a = mid + 1;
-    }
-    topic = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
-    if (a < d.nch) {
-      double acc = 0.0;
-      const uint32_t kb = a * 32u;
-      for (uint32_t q = 0; q < 32; ++q) {
-        const uint32_t k = kb + q;
-        acc = acc + lds_f64(row_s + (k << 3));
-        if (k < d.K && k != K1 && d.alpha * (CP[a] + acc) > y) {
-          topic = k;
-          break;
-        }
-      }
+    const uint32_t t = v - d.Vd;
+    const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, s_run);
+    if (tid == 0) nxt.tnnz[t] = nz;
+    for (uint32_t k = tid; k < d.K; k += blockDim.x) {
+      const uint32_t c = hist[k];
+      if (c) atomicAdd(&nxt.nk[k], (int32_t)c);
     }
   }
-  nxt.z[j] = (uint16_t)topic;
-  atomicAdd(&hist[topic], 1u);
-  rc.sampled += 1;
 }
 
-template <bool kCount>
+// byte offset of the per-warp scratch in the sampler's dynamic shared memory:
+// What' [Kpad] | QP [Kpad] | T [nch] | CP [nch + 1] | hist [Kpad] u32 | (16-aligned) scratch
+__host__ __device__ __forceinline__ uint32_t sampler_ws_offset(uint32_t K) {
+  const uint32_t nch = (K + 31) / 32;
+  const uint32_t b = 2u * nch * 32u * 8u + (2u * nch + 1u) * 8u + nch * 32u * 4u;
+  return (b + 15u) & ~15u;
+}
+
+#ifndef EZLDA_SAMP_MINB
+#define EZLDA_SAMP_MINB 3  // sampler blocks per SM the register allocation must allow
+#endif
+
+// shared memory of the sampler: What' row [Kpad] | CP [nch + 1] (one bulk copy, rs doubles)
+// | T [nch] | hist [Kpad] u32 | kSampWarps x WarpScratch
 __global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* row = reinterpret_cast<double*>(smem);
-  double* T = row + d.Kpad;
+  double* QP = row + d.Kpad;
+  double* T = row + d.rs;
   double* CP = T + d.nch;
   uint32_t* hist = reinterpret_cast<uint32_t*>(CP + d.nch + 1);
-  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(
-      (reinterpret_cast<uintptr_t>(hist + d.Kpad) + 15) & ~(uintptr_t)15);  // kSampWarps entries
+  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(smem + sampler_ws_offset(d.K));
   __shared__ uint32_t s_cursor, s_wsum[32], s_run;
   __shared__ uint32_t s_sampled, s_hitM, s_runs, s_words;
+  __shared__ __align__(8) uint64_t s_mbar;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t item = blockIdx.x;
   const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
   const uint32_t ntok = d.item_ntok[item];
+  const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  const bool dense = v < d.Vd;
+  if (dense && tid == 0) {  // TMA bulk copy of the precomputed What' row + QP
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_s), "r"(1u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    bulk_g2s((uint32_t)__cvta_generic_to_shared(row), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
+  }
   for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
   if (tid == 0) { s_cursor = 0; s_sampled = 0; s_hitM = 0; s_runs = 0; s_words = 0; }
-  WordRec rec;
-  if (!kCount) {
-    rec = d.rec[v];
+  const WordRec rec = d.rec[v];
+  if (dense) {
+    __syncthreads();
+    mbar_wait(mbar_s, 0);
+  } else {
     stage_row(d, cur, v, row);
     if (tid == 0) row[rec.K[0]] = 0.0;  // What'
     __syncthreads();
     chunk_prefix(row, d.nch, T, CP);
-  } else {
-    __syncthreads();
+    q_prefix(row, d.nch, CP, d.alpha, QP);
   }
   RunCounters rc{0, 0, 0, 0};
-  if (kCount) {
-    for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) {
-      const uint32_t j0 = d.run_j0[r], len = d.run_len[r];
-      for (uint32_t t = 0; t < len; ++t) atomicAdd(&hist[cur.z[j0 + t]], 1u);
-    }
-  } else {
+  {
     WarpScratch& ws = s_ws[warp];
     const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
     uint32_t qn = 0;
@@ -657,36 +814,22 @@ __global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(De
         __syncwarp();
       }
       if (qn == 0) break;
-      const uint32_t nb = min(qn, 32u);
-      uint32_t len = 0;
-      if (lane < nb) batch_phase1(d, rec, row_s, ws, lane, ws.q[lane], len, rc);
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= (uint32_t)o) incl += y;
-      }
-      ws.tofs[lane + 1] = incl;
-      if (lane == 0) ws.tofs[0] = 0;
-      const uint32_t ntb = __shfl_sync(kFull, incl, 31);
+      const uint32_t nb = d.segw == 8u ? sample_batch<true>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc)
+                                       : sample_batch<false>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc);
+      // drop the processed runs from the queue
+      const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
+      const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
       __syncwarp();
-      for (uint32_t i = lane; i < ntb; i += 32) batch_token(d, nxt, rec, row_s, CP, hist, ws, i, iter, rc);
-      // drop the processed batch from the queue
-      __syncwarp();
-      {
-        const uint32_t keep = (lane + 32 < qn) ? ws.q[32 + lane] : 0u;
-        __syncwarp();
-        if (lane + 32 < qn) ws.q[lane] = keep;
-      }
+      if (lane + nb < qn) ws.q[lane] = keep0;
+      if (lane + 32u + nb < qn) ws.q[lane + 32u] = keep1;
       qn -= nb;
       __syncwarp();
     }
   }
-  // per-block counters
   {
     const uint32_t smp = warp_sum(rc.sampled), hm = warp_sum(rc.hitM);
     const uint32_t nr = warp_sum(rc.runs), nw = warp_sum(rc.words);
-    if (lane == 0 && !kCount) {
+    if (lane == 0) {
       atomicAdd(&s_sampled, smp);
       atomicAdd(&s_hitM, hm);
       atomicAdd(&s_runs, nr);
@@ -694,32 +837,33 @@ __global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(De
     }
   }
   __syncthreads();
-  if (!kCount && tid == 0) hist[rec.K[0]] += ntok - s_sampled;  // skipped tokens stay at K1
+  if (tid == 0) hist[rec.K[0]] += ntok - s_sampled;  // skipped tokens stay at K1
   __syncthreads();
-  if (v < d.Vd) {
-    int32_t* Wrow = nxt.Wd + (size_t)v * d.K;
-    for (uint32_t k = tid; k < d.K; k += blockDim.x) {
-      const uint32_t c = hist[k];
-      if (c) {
-        atomicAdd(&Wrow[k], (int32_t)c);
-        atomicAdd(&nxt.nk[k], (int32_t)c);
-      }
-    }
-  } else {
-    const uint32_t t = v - d.Vd;
-    const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, &s_run);
-    if (tid == 0) nxt.tnnz[t] = nz;
-    for (uint32_t k = tid; k < d.K; k += blockDim.x) {
-      const uint32_t c = hist[k];
-      if (c) atomicAdd(&nxt.nk[k], (int32_t)c);
-    }
-  }
-  if (!kCount && tid == 0) {
+  item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
+  if (tid == 0) {
     atomicAdd(&d.ctr->sampled, (unsigned long long)s_sampled);
     atomicAdd(&d.ctr->skip_M, (unsigned long long)s_hitM);
     atomicAdd(&d.ctr->active_runs, (unsigned long long)s_runs);
     atomicAdd(&d.ctr->drow_words, (unsigned long long)s_words);
   }
+}
+
+// W / n_k of z (init, set_topics): the item histogram of the current topics.
+__global__ void __launch_bounds__(256) k_wcount(Dev d, Buf cur, Buf nxt) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  __shared__ uint32_t s_wsum[32], s_run;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t item = blockIdx.x;
+  const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
+  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+  __syncthreads();
+  for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) {
+    const uint32_t j0 = d.run_j0[r], len = d.run_len[r];
+    for (uint32_t t = 0; t < len; ++t) atomicAdd(&hist[cur.z[j0 + t]], 1u);
+  }
+  __syncthreads();
+  item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
 }
 
 // ---------------------------------------------------------------------------------
@@ -800,12 +944,13 @@ size_t word_prep_smem_bytes(uint32_t K) {
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-size_t sampler_smem_bytes(uint32_t K) {
-  const uint32_t nch = (K + 31) / 32;
-  size_t b = word_prep_smem_bytes(K) + (size_t)nch * 32 * 4;
-  b = (b + 15) & ~(size_t)15;
-  return b + sizeof(WarpScratch) * kSampWarps;
+uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32; }  // What' | QP
+uint32_t seg_width(uint32_t K) {
+  const uint32_t per = (K + kSegCap - 1) / kSegCap;  // entries per segment so that any row fits
+  return std::max<uint32_t>(8u, (per + 7u) & ~7u);
 }
+size_t sampler_smem_bytes(uint32_t K) { return sampler_ws_offset(K) + sizeof(WarpScratch) * kSampWarps; }
+size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 cudaError_t configure_kernels(uint32_t K) {
@@ -813,8 +958,9 @@ cudaError_t configure_kernels(uint32_t K) {
   const int wp = (int)word_prep_smem_bytes(K), sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = cudaFuncSetAttribute(k_word_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, wp))) return e;
   if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, wp))) return e;
-  if ((e = cudaFuncSetAttribute(k_sampler<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
-  if ((e = cudaFuncSetAttribute(k_sampler<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
+  if ((e = cudaFuncSetAttribute(k_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
+  if ((e = cudaFuncSetAttribute(k_wcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wcount_smem_bytes(K))))
+    return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if (K <= 4096) {
@@ -861,9 +1007,9 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
                     bool count_only, cudaStream_t s) {
   if (!n_items) return;
   if (count_only)
-    k_sampler<true><<<n_items, kSampWarps * 32, sampler_smem_bytes(d.K), s>>>(d, cur, nxt, iteration);
+    k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
-    k_sampler<false><<<n_items, kSampWarps * 32, sampler_smem_bytes(d.K), s>>>(d, cur, nxt, iteration);
+    k_sampler<<<n_items, kSampWarps * 32, sampler_smem_bytes(d.K), s>>>(d, cur, nxt, iteration);
 }
 
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {

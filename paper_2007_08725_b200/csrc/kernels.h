@@ -6,9 +6,11 @@
 //     trid[j] u32  index of the token's run in word-major run order
 //     z[2][j] u16  topics, double-buffered (snapshot semantics)
 //     perm[j] u32  input index of token j (output order only)
-//   dofs[Dn+1] u32 token offsets of docs; D rows at ddb[d] (16-byte aligned, capacity
-//     L_d + 4 rounded up to 4 words; entries start 16-byte aligned after a 4-word header):
-//     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+4+i] = (topic << 16) | count
+//   dofs[Dn+1] u32 token offsets of docs; D rows at ddb[d] (32-byte aligned = one sector,
+//     capacity 8 + roundup8(min(L_d, K)) words; entries start 32-byte aligned after an
+//     8-word header and are zero padded to a multiple of 8 entries, so the sampler reads
+//     whole sectors without masking):
+//     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+8+i] = (topic << 16) | count
 //     sorted by topic (packed CSR; rebuilt every iteration)
 //   word-major runs r in [0, R) (runs of word v contiguous, ordered by doc length desc):
 //     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
@@ -16,6 +18,9 @@
 //   W: dense rows int32 [Vd x K] for words v < Vd, packed sparse tail rows (capacity
 //     min(c_v, K) at tofs[v-Vd]) with tnnz[v-Vd]; double-buffered with n_k[K].
 //   rec[V] WordRec (48 B): top-4 topics/values and Q' of every word.
+//   wrow[Vd][rs] f64: What'[v] (Eq 6: What with the K1 entry zeroed, Kpad entries) followed
+//     by its chunk prefix CP[0..nch] -- written by word-prep, bulk-copied (TMA) into the
+//     sampler's shared memory for dense words.
 //   items: (word, run range, tokens): the sampler's work list, heavy first.
 #pragma once
 #include <cstdint>
@@ -25,7 +30,12 @@
 
 namespace ezl {
 
-constexpr uint32_t kDHdr = 4;  // header words in front of every packed D row
+constexpr uint16_t kUnsampled = 0xFFFFu;  // z^i of a token the sampler must draw (K <= 65535)
+constexpr uint32_t kDHdr = 8;  // header words in front of every packed D row (one 32 B sector)
+#ifndef EZLDA_SEGCAP
+#define EZLDA_SEGCAP 256
+#endif
+constexpr uint32_t kSegCap = EZLDA_SEGCAP;  // sampler: S' segments per warp batch
 
 struct Counters {  // device-side per-iteration counters
   unsigned long long skip_S, skip_M, sampled, active_runs, drow_words, d_nnz;
@@ -34,11 +44,13 @@ struct Counters {  // device-side per-iteration counters
 struct Dev {
   // sizes and parameters
   uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
+  uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
+  uint32_t segw;  // entries per S' segment (multiple of 8; ceil(K / segw) <= kSegCap)
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
   // static structure
   const uint32_t* dofs;
-  const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 4 words)
+  const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 8 words)
   const uint32_t* tw;
   const uint32_t* trid;
   const uint32_t* run_j0;
@@ -54,6 +66,7 @@ struct Dev {
   uint32_t* D;
   uint32_t* flags;
   WordRec* rec;
+  double* wrow;   // [Vd * rs] precomputed What' rows + chunk prefixes (dense words)
   double* den;    // [K] n_k + V beta
   double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
   Counters* ctr;
@@ -85,6 +98,8 @@ void launch_topics_to_input(const uint16_t* z, const uint32_t* perm, uint32_t N,
 void launch_topics_from_input(const uint16_t* in, const uint32_t* perm, uint32_t N, uint16_t* z, cudaStream_t s);
 
 size_t sampler_smem_bytes(uint32_t K);
+uint32_t wrow_stride(uint32_t K);
+uint32_t seg_width(uint32_t K);
 size_t word_prep_smem_bytes(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);
 cudaError_t configure_kernels(uint32_t K);
