@@ -325,6 +325,7 @@ void fill_dev(ezlda* h) {
   d.Vd = h->Vd;
   d.rs = ezl::wrow_stride(h->K);
   d.segw = ezl::seg_width(h->K);
+  d.zmark = h->K <= 32768u ? 1u : 0u;
   d.geff = std::min<uint32_t>(h->g, h->K - 1);
   d.alpha = h->alpha;
   d.beta = h->beta;

@@ -261,7 +261,8 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
       nxt.z[j] = r.K[0];
       ++n_skip;
     } else {
-      nxt.z[j] = kUnsampled;  // the sampler draws it
+      // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
+      nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, 0x7FFFu)) : kUnsampled;
       const uint32_t rid = d.trid[j];
       atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
     }
@@ -470,14 +471,8 @@ struct RunCounters {
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct RunState {  // one per batch slot, shared memory
-  double Sp, M, Z;
-  uint32_t j0, ebase, nnz, soff, nseg, tofs, lastk, C1;
-};
-
 struct __align__(16) WarpScratch {
-  double P[kSegCap];  // segment prefixes of the batch, flattened
-  RunState st[32];
+  double P[2 * kSegCap];  // prefix checkpoints of the batch's runs, flattened (see sample_batch)
   uint32_t q[kQueue];  // queue of flagged runs
 };
 
@@ -494,9 +489,24 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
-// D[d][k] What'[v][k] of one packed entry (topic << 16 | count); padding (0) adds +0.0
+// D[d][k] What'[v][k] of one packed entry (topic << 16 | count); padding (0) adds +0.0.
+// The count is converted exactly with the 2^52 trick (one DADD instead of an I2F.F64).
 __device__ __forceinline__ double entry_term(uint32_t w, uint32_t row_s) {
-  return (double)(w & 0xFFFFu) * lds_f64(row_s + ((w >> 16) << 3));
+  const double c = __hiloint2double(0x43300000, (int)(w & 0xFFFFu)) - 0x1p52;
+  return c * lds_f64(row_s + ((w >> 16) << 3));
+}
+
+// sequential sum of the 8 entries of one sector, continuing acc
+__device__ __forceinline__ double sector_sum(double acc, const uint4& a, const uint4& b, uint32_t row_s) {
+  acc = acc + entry_term(a.x, row_s);
+  acc = acc + entry_term(a.y, row_s);
+  acc = acc + entry_term(a.z, row_s);
+  acc = acc + entry_term(a.w, row_s);
+  acc = acc + entry_term(b.x, row_s);
+  acc = acc + entry_term(b.y, row_s);
+  acc = acc + entry_term(b.z, row_s);
+  acc = acc + entry_term(b.w, row_s);
+  return acc;
 }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
@@ -517,25 +527,41 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar_s, uint32_t parity) {
   } while (!done);
 }
 
+// C1 = D[d][K1] by binary search in the sorted packed row (fallback path: K > 32768 or
+// C1 >= 0x7FFF, where the doc pass cannot carry C1 in the z^i marker).
+__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
+  uint32_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((__ldg(E + mid) >> 16) < k) lo = mid + 1u; else hi = mid;
+  }
+  if (lo < nnz) {
+    const uint32_t w = __ldg(E + lo);
+    if ((w >> 16) == k) return w & 0xFFFFu;
+  }
+  return 0u;
+}
+
 // One batch of flagged runs (warp-uniform control flow).  Returns the number of queue
-// entries consumed.  kSeg8: segw == 8 (one sector per segment; K <= 8 kSegCap).
-template <bool kSeg8>
+// entries consumed.  kSegW: entries per segment (multiple of 16); the per-run state lives
+// in the registers of the run's lane and is fetched by shuffles.
+template <uint32_t kSegW>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, const WordRec& rec, uint32_t row_s,
                                                  const double* QP, uint32_t* hist, WarpScratch& ws, uint32_t qn,
                                                  uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t segw = kSeg8 ? 8u : d.segw;
   const uint32_t K1 = rec.K[0];
-  // ---- A: run table + header, segment admission
+  // ---- A: lane per run: run table + header, segment admission
   const uint32_t nc = min(qn, 32u);
-  uint32_t j0 = 0, dbase = 0, len = 0, hdr = 0, nseg = 0;
+  uint32_t j0 = 0, ebase = 0, len = 0, nnz = 0, nseg = 0;
   if (lane < nc) {
     const uint32_t r = ws.q[lane];
     j0 = d.run_j0[r];
-    dbase = d.run_dbase[r];
+    const uint32_t dbase = d.run_dbase[r];
     len = d.run_len[r];
-    hdr = d.D[dbase];
-    nseg = ((hdr & 0xFFFFu) + segw - 1u) / segw;
+    nnz = d.D[dbase] & 0xFFFFu;
+    ebase = dbase + kDHdr;
+    nseg = (nnz + kSegW - 1u) / kSegW;
   }
   uint32_t sincl = nseg, tincl;
 #pragma unroll
@@ -555,149 +581,163 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, c
   const uint32_t ntb = __shfl_sync(kFull, tincl, 31);
   const uint32_t tofs = tincl - ((lane < nb) ? len : 0u);
   if (lane < nb) {
-    RunState& st = ws.st[lane];
-    st.j0 = j0;
-    st.ebase = dbase + kDHdr;
-    st.nnz = hdr & 0xFFFFu;
-    st.soff = soff;
-    st.nseg = nseg;
-    st.tofs = tofs;
-    st.C1 = 0u;
+    rc.runs += 1;
+    rc.words += 1u + nnz;
   }
-  __syncwarp();
-  // slot of the item with index B0 + lane, items numbered by run: first = per-run start
-  // offsets held by the run lanes (soff / tofs), ascending
+  // slot (run lane) of the item with index B0 + lane; first = per-run start offsets held by
+  // the run lanes (soff / tofs), ascending
   auto slot_of = [&](uint32_t B0, uint32_t first) -> uint32_t {
     const bool inw = lane < nb && first >= B0 && first < B0 + 32u;
     const uint32_t bits = __reduce_or_sync(kFull, inw ? (1u << (first - B0)) : 0u);
     const uint32_t nbefore = __popc(__ballot_sync(kFull, lane < nb && first < B0));
     return nbefore + __popc(bits & (0xFFFFFFFFu >> (31u - lane))) - 1u;
   };
-  // ---- B: lane per segment (one 32-byte sector = 8 entries per load); the next round's
-  //      sector is loaded before this round's terms are computed
-  uint32_t slot_c = 0, e0_c = 0;
-  uint4 qa_c = make_uint4(0u, 0u, 0u, 0u), qb_c = qa_c;
-  const uint32_t* p_c = nullptr;
-  auto locate = [&](uint32_t B0, uint32_t& slot, uint32_t& e0) -> const uint32_t* {
-    slot = slot_of(B0, soff);
-    const RunState& st = ws.st[slot];
-    e0 = (B0 + lane - st.soff) * segw;
-    return d.D + st.ebase + e0;
-  };
-  if (T) {
-    p_c = locate(0, slot_c, e0_c);
-    if (lane < T) ldg256(p_c, qa_c, qb_c);
-  }
+  // ---- B: lane per segment (kSegW entries, 16 = two 32-byte sectors); consecutive lanes
+  //      read consecutive sectors of a row.  The segment sums are combined into the run
+  //      prefixes by a segmented warp scan (carry across rounds).  Checkpoints: kSec
+  //      (kSegW = 16) keeps two per segment, P[2g] = P(before g) + (first sector) and
+  //      P[2g+1] = P(end of g), so a descent walks at most one sector; otherwise P[g] = P(end
+  //      of g).  S' = the run's last checkpoint.
+  constexpr bool kSec = kSegW == 16u;
+  double carry = 0.0;
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
-    uint32_t slot_n = 0, e0_n = 0;
-    uint4 qa_n = make_uint4(0u, 0u, 0u, 0u), qb_n = qa_n;
-    const uint32_t* p_n = nullptr;
-    if (B0 + 32u < T) {
-      p_n = locate(B0 + 32u, slot_n, e0_n);
-      if (B0 + 32u + lane < T) ldg256(p_n, qa_n, qb_n);
-    }
-    if (B0 + lane < T) {
-      const uint32_t nnz = ws.st[slot_c].nnz;
-      double acc = 0.0;
-      for (uint32_t b = 0; kSeg8 || (b < segw && e0_c + b < nnz); b += 8u) {
-        if (b) ldg256(p_c + b, qa_c, qb_c);
-        acc = acc + entry_term(qa_c.x, row_s);
-        acc = acc + entry_term(qa_c.y, row_s);
-        acc = acc + entry_term(qa_c.z, row_s);
-        acc = acc + entry_term(qa_c.w, row_s);
-        acc = acc + entry_term(qb_c.x, row_s);
-        acc = acc + entry_term(qb_c.y, row_s);
-        acc = acc + entry_term(qb_c.z, row_s);
-        acc = acc + entry_term(qb_c.w, row_s);
-        // C1 = D[d][K1] (Eq 8): found by the lane whose sorted topics bracket K1
-        const uint32_t hi = (e0_c + b + 8u <= nnz) ? (qb_c.w >> 16) : 0xFFFFu;
-        if ((qa_c.x >> 16) <= K1 && K1 <= hi) {
-          const uint32_t w[8] = {qa_c.x, qa_c.y, qa_c.z, qa_c.w, qb_c.x, qb_c.y, qb_c.z, qb_c.w};
+    const uint32_t g = B0 + lane;
+    const uint32_t slot = slot_of(B0, soff);
+    const uint32_t s_soff = __shfl_sync(kFull, soff, slot);
+    const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
+    const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
+    const uint32_t e0 = (g - s_soff) * kSegW;
+    const uint32_t* p = d.D + s_ebase + e0;
+    double acc = 0.0, acc8 = 0.0;
+    if (g < T) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if ((w[i] >> 16) == K1 && (w[i] & 0xFFFFu)) ws.st[slot_c].C1 = w[i] & 0xFFFFu;
-        }
-        if (kSeg8) break;
+      for (uint32_t b = 0; b < kSegW; b += 16u) {
+        uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
+        if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
+        if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
+        acc = sector_sum(acc, qa, qb, row_s);
+        if (kSec) acc8 = acc;
+        acc = sector_sum(acc, qc, qd, row_s);
       }
-      ws.P[B0 + lane] = acc;
     }
-    slot_c = slot_n;
-    e0_c = e0_n;
-    p_c = p_n;
-    qa_c = qa_n;
-    qb_c = qb_n;
+    // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
+    const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(kFull, acc, o);
+      if (lane >= rs + (uint32_t)o) acc = y + acc;
+    }
+    const bool cont = s_soff < B0;  // the run started in an earlier round
+    if (cont) acc = carry + acc;
+    if (kSec) {
+      double excl = __shfl_up_sync(kFull, acc, 1);
+      if (lane == rs) excl = cont ? carry : 0.0;
+      if (g < T) {
+        ws.P[2u * g] = excl + acc8;
+        ws.P[2u * g + 1u] = acc;
+      }
+    } else if (g < T) {
+      ws.P[g] = acc;
+    }
+    carry = __shfl_sync(kFull, acc, 31);
   }
   __syncwarp();
-  // ---- C: lane per run
-  if (lane < nb) {
-    RunState& st = ws.st[lane];
-    double acc = 0.0;
-    for (uint32_t s = soff; s < soff + nseg; ++s) {
-      acc = acc + ws.P[s];
-      ws.P[s] = acc;
-    }
-    const uint32_t nnz = st.nnz;
-    const uint32_t* E = d.D + st.ebase;
-    uint32_t lastk = K1;  // last topic of the row other than K1
-    if (nnz) {
-      const uint32_t kl = __ldg(E + nnz - 1) >> 16;
-      lastk = (kl != K1) ? kl : (nnz >= 2 ? (__ldg(E + nnz - 2) >> 16) : K1);
-    }
-    st.Sp = acc;
-    st.M = mpt_M(rec, st.C1, d.alpha);
-    st.Z = (st.M + acc) + rec.Qp;
-    st.lastk = lastk;
-    rc.runs += 1;
-    rc.words += 1u + nnz;
-  }
-  __syncwarp();
-  // ---- D: lane per token; the doc pass left kUnsampled in z^i for the tokens that failed
-  //      the MPT test (the others already hold K1)
+  // ---- D: lane per token.  The doc pass left a marker in z^i for the tokens that failed
+  //      the MPT test (the others already hold K1): 0x8000 | min(C1, 0x7FFF) when K <=
+  //      32768 (d.zmark), else 0xFFFF.
+  const double Qp = rec.Qp;
   for (uint32_t B0 = 0; B0 < ntb; B0 += 32u) {
     const uint32_t slot = slot_of(B0, tofs);
+    const uint32_t s_j0 = __shfl_sync(kFull, j0, slot);
+    const uint32_t s_tofs = __shfl_sync(kFull, tofs, slot);
+    const uint32_t s_soff = __shfl_sync(kFull, soff, slot);
+    const uint32_t s_nseg = __shfl_sync(kFull, nseg, slot);
+    const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
+    const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
     const uint32_t i = B0 + lane;
     if (i >= ntb) continue;
-    const RunState& st = ws.st[slot];
-    const uint32_t j = st.j0 + (i - st.tofs);
-    if (nxt.z[j] != kUnsampled) continue;  // skipped by the MPT test
+    const uint32_t j = s_j0 + (i - s_tofs);
+    const uint32_t zm = nxt.z[j];
+    uint32_t C1;
+    if (d.zmark) {
+      if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
+      C1 = zm & 0x7FFFu;
+      if (C1 == 0x7FFFu) C1 = row_count(d.D + s_ebase, s_nnz, K1);
+    } else {
+      if (zm != kUnsampled) continue;
+      C1 = row_count(d.D + s_ebase, s_nnz, K1);
+    }
+    constexpr uint32_t kCk = kSec ? 2u : 1u;  // checkpoints per segment
+    const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
+    const double Sp = nck ? ws.P[c0 + nck - 1u] : 0.0;
+    const double M = mpt_M(rec, C1, d.alpha);
+    const double Z = (M + Sp) + Qp;
     const double u = philox_u(d.seed, iter, d.token_base + j);
-    const double x = u * st.Z;
+    const double x = u * Z;
     uint32_t topic;
-    if (x < st.M) {
+    if (x < M) {
       topic = K1;  // second chance: u < M / (M + S' + Q')
       rc.hitM += 1;
-    } else if (x < st.M + st.Sp) {
-      // S' branch: first segment with P > y, then the walk inside it
-      const double y = x - st.M;
-      uint32_t a = st.soff, b = st.soff + st.nseg - 1u;
+    } else if (x < M + Sp) {
+      // S' branch: first checkpoint with P > y, then the walk from the previous one
+      const double y = x - M;
+      uint32_t a = c0, b = c0 + nck - 1u;
       while (a < b) {
         const uint32_t mid = (a + b) >> 1;
         if (ws.P[mid] > y) b = mid; else a = mid + 1u;
       }
-      const double base = (a > st.soff) ? ws.P[a - 1u] : 0.0;
-      const uint32_t e0 = (a - st.soff) * segw;
-      const uint32_t e1 = min(e0 + segw, st.nnz);
-      const uint32_t* E = d.D + st.ebase;
-      double acc = 0.0;
+      const double base = (a > c0) ? ws.P[a - 1u] : 0.0;
+      const uint32_t* E = d.D + s_ebase;
       uint32_t last = 0xFFFFFFFFu;
       topic = 0xFFFFFFFFu;
-      for (uint32_t e = e0; e < e1; ++e) {
-        const uint32_t w = __ldg(E + e);
-        const uint32_t k = w >> 16;
-        acc = acc + entry_term(w, row_s);
-        if (k != K1) {
-          last = k;
-          if (base + acc > y) {
-            topic = k;
-            break;
+      if (kSec) {  // one sector (8 entries; zero padding past nnz) from registers
+        uint4 qa, qb;
+        ldg256(E + (a - c0) * 8u, qa, qb);
+        const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t w = wv[e];
+          if (topic == 0xFFFFFFFFu && w != 0u) {
+            const uint32_t k = w >> 16;
+            acc = acc + entry_term(w, row_s);
+            if (k != K1) {
+              last = k;
+              if (base + acc > y) topic = k;
+            }
+          }
+        }
+      } else {
+        const uint32_t e0 = (a - c0) * kSegW;
+        const uint32_t e1 = min(e0 + kSegW, s_nnz);
+        double acc = 0.0;
+        for (uint32_t e = e0; e < e1; ++e) {
+          const uint32_t w = __ldg(E + e);
+          const uint32_t k = w >> 16;
+          acc = acc + entry_term(w, row_s);
+          if (k != K1) {
+            last = k;
+            if (base + acc > y) {
+              topic = k;
+              break;
+            }
           }
         }
       }
-      if (topic == 0xFFFFFFFFu) topic = (last != 0xFFFFFFFFu) ? last : st.lastk;  // rounding at S' end
+      if (topic == 0xFFFFFFFFu) {  // rounding at the end of the walk / of S'
+        if (last == 0xFFFFFFFFu) {  // the walked entries hold K1 only: last topic != K1 of the row
+          for (uint32_t e = s_nnz; e-- > 0;) {
+            const uint32_t k = __ldg(E + e) >> 16;
+            if (k != K1) { last = k; break; }
+          }
+          if (last == 0xFFFFFFFFu) last = K1;
+        }
+        topic = last;
+      }
     } else {
       // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
       // is flat across K1); none -> last topic != K1
-      const double y = (x - st.M) - st.Sp;
+      const double y = (x - M) - Sp;
       uint32_t a = 0, b = d.Kpad - 1u;
       while (a < b) {
         const uint32_t mid = (a + b) >> 1;
@@ -814,8 +854,14 @@ __global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(De
         __syncwarp();
       }
       if (qn == 0) break;
-      const uint32_t nb = d.segw == 8u ? sample_batch<true>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc)
-                                       : sample_batch<false>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc);
+      uint32_t nb;
+      switch (d.segw) {
+        case 16u: nb = sample_batch<16u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 32u: nb = sample_batch<32u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 64u: nb = sample_batch<64u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 128u: nb = sample_batch<128u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
+        default: nb = sample_batch<256u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
+      }
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
       const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
@@ -945,9 +991,10 @@ size_t word_prep_smem_bytes(uint32_t K) {
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
 uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32; }  // What' | QP
-uint32_t seg_width(uint32_t K) {
-  const uint32_t per = (K + kSegCap - 1) / kSegCap;  // entries per segment so that any row fits
-  return std::max<uint32_t>(8u, (per + 7u) & ~7u);
+uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= 16 with K <= kSegCap segw
+  uint32_t w = 16u;
+  while (w * kSegCap < K) w <<= 1;
+  return w;
 }
 size_t sampler_smem_bytes(uint32_t K) { return sampler_ws_offset(K) + sizeof(WarpScratch) * kSampWarps; }
 size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }

@@ -44,8 +44,9 @@ struct Counters {  // device-side per-iteration counters
 struct Dev {
   // sizes and parameters
   uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
+  uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, 0x7FFF)
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
-  uint32_t segw;  // entries per S' segment (multiple of 8; ceil(K / segw) <= kSegCap)
+  uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
   // static structure
