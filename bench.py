@@ -280,6 +280,7 @@ def main():
         "phases_ms_per_step": {"wordprep": S["ms_wordprep"] / args.steps, "docpass": S["ms_docpass"] / args.steps,
                                "sample": S["ms_sample"] / args.steps, "allreduce": S["ms_allreduce"] / args.steps},
         "skip_S_frac": S["skip_S"] / max(S["n_tokens"], 1), "skip_final_frac": S["skip_final"] / max(S["n_tokens"], 1),
+        "exact_redraw_frac": S["exact_redraws"] / max(S["sampled"], 1),
         "llpt_after": llpt, "setup_s": {"generate": gen_s, "create": create_s},
     }
     with_clk = clk.summary()

@@ -32,8 +32,9 @@
  *     and the stream given in the options (or one it creates).
  *   - Threading: one handle per host thread; calls on a handle are serialised.
  *   - Limits (16+16-bit packing): K <= 65535, doc length <= 65535,
- *     tokens per shard < 2^32.  This build additionally requires K <= 16384
- *     (the staged fp64 What row must fit in shared memory; NEXT-2 lifts it).
+ *     tokens per shard < 2^32.  This build additionally requires K <= 11200
+ *     (the staged fp32 What' row and fp64 Q' table of a sampler item must fit in
+ *     shared memory; NEXT-2 lifts it).
  */
 #ifndef EZLDA_H
 #define EZLDA_H
@@ -78,6 +79,8 @@ typedef struct {
   uint32_t doc_block_kb;     /* L2 tiling: cut hot-word sampler items at doc windows of     */
                              /* this many KiB of D rows, run them window-major;            */
                              /* 0 -> 32768 (32 MiB); 0xFFFFFFFF -> one window (off)        */
+  uint32_t exact_draws;      /* 1: skip the fp32 fast path, draw every sampled token in fp64 */
+                             /* (identical topics by construction; test / ablation knob)   */
 } ezlda_options;
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL
@@ -110,6 +113,8 @@ typedef struct {
   double model_bytes_sample; /* ... of the sampler kernel alone                            */
   double model_bytes_docpass;/* ... of the doc-pass kernels                                */
   uint64_t kernel_launches;  /* library kernels launched by the iteration                  */
+  uint64_t exact_redraws;    /* sampled tokens redrawn on the exact fp64 path (fp32 decision
+                                not certified by its error margin)      */
 } ezlda_iter_stats;
 
 /* Build the resident corpus and draw z^0 (iteration 0).

@@ -239,6 +239,7 @@ struct ezlda {
   std::vector<int> pending;  // FIFO of slot indices not yet folded
   uint64_t slot_counter = 0;
   ezl::Counters* ctr_host = nullptr;  // pinned, kSlots entries
+  uint32_t exact_all = 0;             // options.exact_draws
   ezlda_iter_stats sum{};
   uint32_t sum_n = 0;
   double* llpt_partial = nullptr;
@@ -326,6 +327,8 @@ void fill_dev(ezlda* h) {
   d.rs = ezl::wrow_stride(h->K);
   d.segw = ezl::seg_width(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
+  d.nslots = ezl::sampler_slots(h->K);
+  d.exact_all = h->exact_all;
   d.geff = std::min<uint32_t>(h->g, h->K - 1);
   d.alpha = h->alpha;
   d.beta = h->beta;
@@ -642,7 +645,10 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
-  EZ_ALLOC(h, d.wrow, double, (size_t)h->Vd * d.rs);
+  // What' | QP rows for every word when they fit in 8 GiB (the sampler then stages every
+  // item with one bulk copy), else for the dense words only (tail rows staged by a warp)
+  d.Vw = ((uint64_t)h->V * d.rs * 8ull <= (8ull << 30)) ? h->V : h->Vd;
+  EZ_ALLOC(h, d.wrow, double, (size_t)d.Vw * d.rs);
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
   EZ_ALLOC(h, d.ctr, ezl::Counters, 1);
@@ -694,6 +700,7 @@ ezlda_status fold_one(ezlda* h) {
   st.drow_words = c.drow_words;
   st.d_nnz = c.d_nnz;
   st.kernel_launches = sl.launches;
+  st.exact_redraws = c.exact;
   if (h->timing) {
     float a = 0, b = 0, cc = 0, dd = 0;
     EZ_CUDA(h, cudaEventElapsedTime(&a, sl.ev[0], sl.ev[1]));
@@ -737,6 +744,7 @@ ezlda_status fold_one(ezlda* h) {
   S.model_bytes_sample += st.model_bytes_sample;
   S.model_bytes_docpass += st.model_bytes_docpass;
   S.kernel_launches += st.kernel_launches;
+  S.exact_redraws += st.exact_redraws;
   h->sum_n += 1;
   return EZLDA_OK;
 }
@@ -769,10 +777,14 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   if (n_tokens == 0 || K == 0 || V == 0 || n_docs == 0) return bad(EZLDA_E_INVALID, "n_tokens, K, V and n_docs must be > 0");
   if (!(alpha > 0.0) || !(beta > 0.0)) return bad(EZLDA_E_INVALID, "alpha and beta must be > 0");
   if (K > 65535) return bad(EZLDA_E_RANGE, "K > 65535 (16-bit topic packing, P:753)");
-  if (K > 16384) return bad(EZLDA_E_RANGE, "K > 16384 not supported by this build (NEXT-2)");
+  if (ezl::sampler_slots(K) == 0)
+    return bad(EZLDA_E_RANGE, "K > 11200 not supported by this build (staged What' row + Q' table, NEXT-2)");
   if (n_tokens >= (1ull << 32)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^32 per shard");
   ezlda_options o{};
-  if (opts) o = *opts;
+  if (opts) {  // struct_size versioning: a smaller (older) struct leaves the new fields zero
+    const size_t n = opts->struct_size ? std::min<size_t>(opts->struct_size, sizeof(o)) : sizeof(o);
+    std::memcpy(&o, opts, n);
+  }
   if (o.g > 3) return bad(EZLDA_E_INVALID, "g must be in {1,2,3} (0 = default 2)");
   if (o.w_mode > 2) return bad(EZLDA_E_INVALID, "unknown w_mode");
   ezlda* h = new (std::nothrow) ezlda();
@@ -788,6 +800,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   h->rank = o.rank;
   h->world = o.world > 1 ? o.world : 1;
   h->timing = !o.no_phase_timing;
+  h->exact_all = o.exact_draws ? 1u : 0u;
   h->dev.token_base = o.token_base;
   ezlda_status st = EZLDA_OK;
   if (o.stream) {

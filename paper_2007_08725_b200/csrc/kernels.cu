@@ -24,7 +24,6 @@ namespace {
 
 constexpr int kDocWarpCap = 512; // doc-pass warp tier: documents up to 512 tokens
 constexpr int kDocWarps = 8;
-constexpr int kSampWarps = 8;
 constexpr int kLlptWarps = 8;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -79,20 +78,6 @@ __device__ void chunk_prefix(const double* row, uint32_t nch, double* T, double*
     for (uint32_t c = 0; c < nch; ++c) {
       acc = acc + T[c];
       CP[c + 1] = acc;
-    }
-  }
-  __syncthreads();
-}
-
-// Q' prefix table of a staged What' row: QP[k] = alpha * P(k) with P(k) as above (the
-// chunk prefix CP[k/32] plus the sequential sum inside the chunk).  QP is non-decreasing
-// and QP[Kpad-1] = alpha CP[nch] = Q'; the Q' descent becomes one binary search.
-__device__ void q_prefix(const double* row, uint32_t nch, const double* CP, double alpha, double* QP) {
-  for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
-    double acc = 0.0;
-    for (uint32_t t = 0; t < 32; ++t) {
-      acc = acc + row[c * 32 + t];
-      QP[c * 32 + t] = alpha * (CP[c] + acc);
     }
   }
   __syncthreads();
@@ -189,8 +174,7 @@ __global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
   if (d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard
   extern __shared__ __align__(16) unsigned char smem[];
   double* row = reinterpret_cast<double*>(smem);
-  double* T = row + d.Kpad;
-  double* CP = T + d.nch;
+  double* QPs = row + d.Kpad;
   __shared__ double s_v[4][4];
   __shared__ uint32_t s_k[4][4];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -215,17 +199,39 @@ __global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
       r.a[i] = ok ? f.v[i] : 0.0;
       r.K[i] = ok ? (uint16_t)f.k[i] : (uint16_t)0;
     }
-    r.Qp = 0.0;
-    d.rec[v] = r;
     row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
+    // Q' prefix P_v(k) = sum_{j <= k, j != K1} What[j], ascending and strictly sequential:
+    // the oracle's order, so QP[k] = alpha P_v(k) and Q' = alpha P_v(K-1) are its values bit
+    // for bit (padding past K adds +0.0)
+    // the loads of a 16-entry chunk are issued before the previous chunk's dependent adds
+    double acc = 0.0, x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = row[i];
+    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 16u) {  // Kpad is a multiple of 32
+      double xn[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) xn[i] = (k0 + 16u < d.Kpad) ? row[k0 + 16u + i] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc = acc + x[i];
+        QPs[k0 + i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = xn[i];
+    }
+    r.Qp = d.alpha * QPs[d.K - 1];
+    d.rec[v] = r;
   }
   __syncthreads();
-  chunk_prefix(row, d.nch, T, CP);
-  if (tid == 0) d.rec[v].Qp = d.alpha * CP[d.nch];
-  if (v < d.Vd) {  // What'[v] | QP for the sampler's bulk copy (dense words)
-    double* out = d.wrow + (size_t)v * d.rs;
-    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) out[k] = row[k];
-    q_prefix(row, d.nch, CP, d.alpha, out + d.Kpad);
+  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) QPs[k] = d.alpha * QPs[k];
+  __syncthreads();
+  if (v < d.Vw) {  // fp32 What'[v] | QP for the sampler's bulk copy
+    float* outf = reinterpret_cast<float*>(d.wrow + (size_t)v * d.rs);
+    double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
+    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) {
+      outf[k] = (float)row[k];
+      outq[k] = QPs[k];
+    }
   }
 }
 
@@ -466,14 +472,14 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
 // The S' prefix is a two-level (segment, entry) sum, like the Q' prefix: it differs from
 // the oracle's single sequential sum by rounding only.
 struct RunCounters {
-  uint32_t sampled, hitM, runs, words;
+  uint32_t sampled, hitM, runs, words, exact;
 };
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
 struct __align__(16) WarpScratch {
   double P[2 * kSegCap];  // prefix checkpoints of the batch's runs, flattened (see sample_batch)
-  uint32_t q[kQueue];  // queue of flagged runs
+  uint32_t q[kQueue];     // queue of flagged runs
 };
 
 // 32-byte (one sector) read-only load
@@ -483,29 +489,36 @@ __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& a, uint4& b) {
                : "l"(p));
 }
 
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 
-// D[d][k] What'[v][k] of one packed entry (topic << 16 | count); padding (0) adds +0.0.
-// The count is converted exactly with the 2^52 trick (one DADD instead of an I2F.F64).
-__device__ __forceinline__ double entry_term(uint32_t w, uint32_t row_s) {
-  const double c = __hiloint2double(0x43300000, (int)(w & 0xFFFFu)) - 0x1p52;
-  return c * lds_f64(row_s + ((w >> 16) << 3));
+// fp32 bit pattern -> the same value in fp64, exact for positive normal floats (three
+// integer ops instead of an F2F conversion); +0.0f maps to 2^-127, which the certification
+// margin of sample_batch absorbs
+__device__ __forceinline__ double f32bits_to_f64(uint32_t f) {
+  return __hiloint2double((int)((f >> 3) + 0x38000000u), (int)(f << 29));
 }
 
-// sequential sum of the 8 entries of one sector, continuing acc
+// acc + D[d][k] What'_f32[v][k] for one packed entry (topic << 16 | count): the product is
+// exact in fp64 (16 x 24 bits), one rounding per entry (DFMA); the count converts exactly
+// with the 2^52 trick; padding (0) adds +0.
+__device__ __forceinline__ double entry_fma(uint32_t w, uint32_t row_s, double acc) {
+  const double c = __hiloint2double(0x43300000, (int)(w & 0xFFFFu)) - 0x1p52;
+  return __fma_rn(c, f32bits_to_f64(lds_u32(row_s + ((w >> 16) << 2))), acc);
+}
+
 __device__ __forceinline__ double sector_sum(double acc, const uint4& a, const uint4& b, uint32_t row_s) {
-  acc = acc + entry_term(a.x, row_s);
-  acc = acc + entry_term(a.y, row_s);
-  acc = acc + entry_term(a.z, row_s);
-  acc = acc + entry_term(a.w, row_s);
-  acc = acc + entry_term(b.x, row_s);
-  acc = acc + entry_term(b.y, row_s);
-  acc = acc + entry_term(b.z, row_s);
-  acc = acc + entry_term(b.w, row_s);
+  acc = entry_fma(a.x, row_s, acc);
+  acc = entry_fma(a.y, row_s, acc);
+  acc = entry_fma(a.z, row_s, acc);
+  acc = entry_fma(a.w, row_s, acc);
+  acc = entry_fma(b.x, row_s, acc);
+  acc = entry_fma(b.y, row_s, acc);
+  acc = entry_fma(b.z, row_s, acc);
+  acc = entry_fma(b.w, row_s, acc);
   return acc;
 }
 
@@ -542,13 +555,78 @@ __device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, u
   return 0u;
 }
 
+// What[v][k] in fp64 exactly as word-prep / the oracle form it: (W[v][k] + beta) / den_k.
+__device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint32_t v, uint32_t k) {
+  uint32_t c;
+  if (v < d.Vd) {
+    c = (uint32_t)cur.Wd[(size_t)v * d.K + k];
+  } else {
+    const uint32_t t = v - d.Vd;
+    const uint32_t* tr = cur.Wt + d.tofs[t];
+    c = row_count(tr, cur.tnnz[t], k);
+  }
+  return ((double)c + d.beta) / d.den[k];
+}
+
+// The oracle's per-token draw in fp64 with its summation orders:
+// S' = ascending sequential sum over the row's topics != K1 of D[d][k] What[v][k], Z = (M +
+// S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fp32 fast
+// path could not certify its decision.
+__device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, const uint32_t* E,
+                               uint32_t nnz, double M, double u, const double* QP, bool& hitM) {
+  const uint32_t K1 = rec.K[0];
+  double Sp = 0.0;
+#pragma unroll 4
+  for (uint32_t e = 0; e < nnz; ++e) {
+    const uint32_t w = __ldg(E + e);
+    const uint32_t k = w >> 16;
+    if (k != K1) Sp = Sp + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
+  }
+  const double Z = (M + Sp) + rec.Qp;
+  const double x = u * Z;
+  hitM = false;
+  if (x < M) {
+    hitM = true;
+    return K1;
+  }
+  if (x < M + Sp) {
+    const double y = x - M;
+    double acc = 0.0;
+    uint32_t last = K1;
+    for (uint32_t e = 0; e < nnz; ++e) {
+      const uint32_t w = __ldg(E + e);
+      const uint32_t k = w >> 16;
+      if (k == K1) continue;
+      acc = acc + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
+      last = k;
+      if (acc > y) return k;
+    }
+    return last;
+  }
+  const double y = (x - M) - Sp;
+  uint32_t a = 0, b = d.Kpad - 1u;
+  while (a < b) {
+    const uint32_t mid = (a + b) >> 1;
+    if (QP[mid] > y) b = mid; else a = mid + 1u;
+  }
+  if (a == K1 && QP[a] > y) ++a;  // only when K1 = 0 and y < 0
+  if (a >= d.K || !(QP[a] > y)) a = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
+  return a;
+}
+
 // One batch of flagged runs (warp-uniform control flow).  Returns the number of queue
 // entries consumed.  kSegW: entries per segment (multiple of 16); the per-run state lives
 // in the registers of the run's lane and is fetched by shuffles.
+//
+// Precision: the S' sums use the fp32 copy of What' (half the shared-memory gather
+// traffic) with fp32 FMA accumulation.  Every decision of the fast path (x vs M, x vs
+// M + S', the S' and Q' descents) is taken only if it holds with a margin that bounds the
+// fp32 error (relative (nnz + 16) 2^-23 of S', far above fp64 rounding); otherwise the token
+// is redrawn by exact_draw.  Either way the topic equals the oracle's fp64 decision.
 template <uint32_t kSegW>
-__device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, const WordRec& rec, uint32_t row_s,
-                                                 const double* QP, uint32_t* hist, WarpScratch& ws, uint32_t qn,
-                                                 uint32_t iter, RunCounters& rc) {
+__device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
+                                                 uint32_t v, uint32_t row_s, const double* QP, uint32_t* hist,
+                                                 WarpScratch& ws, uint32_t qn, uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
   // ---- A: lane per run: run table + header, segment admission
@@ -658,14 +736,15 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, c
     if (i >= ntb) continue;
     const uint32_t j = s_j0 + (i - s_tofs);
     const uint32_t zm = nxt.z[j];
+    const uint32_t* E = d.D + s_ebase;
     uint32_t C1;
     if (d.zmark) {
       if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
       C1 = zm & 0x7FFFu;
-      if (C1 == 0x7FFFu) C1 = row_count(d.D + s_ebase, s_nnz, K1);
+      if (C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
     } else {
       if (zm != kUnsampled) continue;
-      C1 = row_count(d.D + s_ebase, s_nnz, K1);
+      C1 = row_count(E, s_nnz, K1);
     }
     constexpr uint32_t kCk = kSec ? 2u : 1u;  // checkpoints per segment
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
@@ -674,79 +753,78 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, c
     const double Z = (M + Sp) + Qp;
     const double u = philox_u(d.seed, iter, d.token_base + j);
     const double x = u * Z;
-    uint32_t topic;
-    if (x < M) {
-      topic = K1;  // second chance: u < M / (M + S' + Q')
-      rc.hitM += 1;
-    } else if (x < M + Sp) {
-      // S' branch: first checkpoint with P > y, then the walk from the previous one
-      const double y = x - M;
-      uint32_t a = c0, b = c0 + nck - 1u;
-      while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (ws.P[mid] > y) b = mid; else a = mid + 1u;
-      }
-      const double base = (a > c0) ? ws.P[a - 1u] : 0.0;
-      const uint32_t* E = d.D + s_ebase;
-      uint32_t last = 0xFFFFFFFFu;
-      topic = 0xFFFFFFFFu;
-      if (kSec) {  // one sector (8 entries; zero padding past nnz) from registers
-        uint4 qa, qb;
-        ldg256(E + (a - c0) * 8u, qa, qb);
-        const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-        double acc = 0.0;
+    // certification margin: every prefix P~ of the fast path satisfies |P~ - P| <= (2^-24 +
+    // (nnz + 48) 2^-53) S' (fp32 rounding of What', one fp64 rounding per entry / scan level
+    // / carry / walk step); x and y inherit it at most twice; 4e-15 Z covers the fp64
+    // roundings of M, Z, x and the oracle's own sums
+    const double mg = 2.0 * (5.9604644775390625e-8 + (double)(s_nnz + 48u) * 1.1102230246251565e-16) * Sp + 4e-15 * Z;
+    uint32_t topic = 0xFFFFFFFFu;
+    bool hit = false;
+    if (!d.exact_all && fabs(x - M) > mg && fabs(x - (M + Sp)) > mg) {
+      if (x < M) {
+        topic = K1;  // second chance: u < M / (M + S' + Q')
+        hit = true;
+      } else if (x < M + Sp) {
+        // S' branch: first checkpoint with P > y, then the walk from the previous one
+        const double y = x - M;
+        uint32_t a = c0, b = c0 + nck - 1u;
+        while (a < b) {
+          const uint32_t mid = (a + b) >> 1;
+          if (ws.P[mid] > y) b = mid; else a = mid + 1u;
+        }
+        const double base = (a > c0) ? ws.P[a - 1u] : 0.0;
+        double pb = base;  // prefix before the candidate entry
+        if (kSec) {  // one sector (8 entries; zero padding past nnz) from registers
+          uint4 qa, qb;
+          ldg256(E + (a - c0) * 8u, qa, qb);
+          const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+          double acc = 0.0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t w = wv[e];
-          if (topic == 0xFFFFFFFFu && w != 0u) {
-            const uint32_t k = w >> 16;
-            acc = acc + entry_term(w, row_s);
-            if (k != K1) {
-              last = k;
-              if (base + acc > y) topic = k;
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t w = wv[e];
+            if (topic == 0xFFFFFFFFu && w != 0u) {
+              acc = entry_fma(w, row_s, acc);
+              const double pa = base + acc;
+              if ((w >> 16) != K1 && pa > y) {
+                topic = (pa - y > mg && y - pb > mg) ? (w >> 16) : 0xFFFFFFFEu;
+              }
+              pb = pa;
             }
           }
-        }
-      } else {
-        const uint32_t e0 = (a - c0) * kSegW;
-        const uint32_t e1 = min(e0 + kSegW, s_nnz);
-        double acc = 0.0;
-        for (uint32_t e = e0; e < e1; ++e) {
-          const uint32_t w = __ldg(E + e);
-          const uint32_t k = w >> 16;
-          acc = acc + entry_term(w, row_s);
-          if (k != K1) {
-            last = k;
-            if (base + acc > y) {
-              topic = k;
+        } else {
+          const uint32_t e0 = (a - c0) * kSegW;
+          const uint32_t e1 = min(e0 + kSegW, s_nnz);
+          double acc = 0.0;
+          for (uint32_t e = e0; e < e1; ++e) {
+            const uint32_t w = __ldg(E + e);
+            acc = entry_fma(w, row_s, acc);
+            const double pa = base + acc;
+            if ((w >> 16) != K1 && pa > y) {
+              topic = (pa - y > mg && y - pb > mg) ? (w >> 16) : 0xFFFFFFFEu;
               break;
             }
+            pb = pa;
           }
         }
-      }
-      if (topic == 0xFFFFFFFFu) {  // rounding at the end of the walk / of S'
-        if (last == 0xFFFFFFFFu) {  // the walked entries hold K1 only: last topic != K1 of the row
-          for (uint32_t e = s_nnz; e-- > 0;) {
-            const uint32_t k = __ldg(E + e) >> 16;
-            if (k != K1) { last = k; break; }
-          }
-          if (last == 0xFFFFFFFFu) last = K1;
+        if (topic == 0xFFFFFFFEu) topic = 0xFFFFFFFFu;  // uncertified: exact redraw
+      } else {
+        // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
+        // is flat across K1 and holds the oracle's values)
+        const double y = (x - M) - Sp;
+        uint32_t a = 0, b = d.Kpad - 1u;
+        while (a < b) {
+          const uint32_t mid = (a + b) >> 1;
+          if (QP[mid] > y) b = mid; else a = mid + 1u;
         }
-        topic = last;
+        const double prev = a ? QP[a - 1u] : 0.0;
+        if (a != K1 && a < d.K && QP[a] - y > mg && y - prev > mg) topic = a;
       }
-    } else {
-      // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
-      // is flat across K1); none -> last topic != K1
-      const double y = (x - M) - Sp;
-      uint32_t a = 0, b = d.Kpad - 1u;
-      while (a < b) {
-        const uint32_t mid = (a + b) >> 1;
-        if (QP[mid] > y) b = mid; else a = mid + 1u;
-      }
-      if (a == K1 && QP[a] > y) ++a;  // only when K1 = 0 and y < 0
-      if (a >= d.K || !(QP[a] > y)) a = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
-      topic = a;
     }
+    if (topic == 0xFFFFFFFFu) {
+      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, QP, hit);
+      rc.exact += 1;
+    }
+    if (hit) rc.hitM += 1;
     nxt.z[j] = (uint16_t)topic;
     atomicAdd(&hist[topic], 1u);
     rc.sampled += 1;
@@ -755,8 +833,292 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& nxt, c
   return nb;
 }
 
-// W / n_k of one item from its topic histogram (dense rows: atomics, the item may be one
-// of several regions of the word; tail rows: ordered compaction into the packed row).
+// ---------------------------------------------------------------------------------
+// Persistent, slot-pipelined sampler.  One block per SM (kSampWarps warps) loops over the
+// global heavy-first item list.  The block's k-th item lives in slot k % kSlots (What'
+// row + QP, topic histogram, cursor, counters).  Every warp walks the block's items in
+// order and leaves an item as soon as its run cursor is exhausted; the LAST warp to leave
+// item k writes its W row / n_k (warp-level epilogue) and re-arms the slot with block
+// item k + kSlots (claim from the global counter, TMA bulk copy of a dense What' row or a
+// warp-staged tail row).  No block-wide barrier after the prologue: a warp is never idle
+// while another warp finishes the previous item.
+// ---------------------------------------------------------------------------------
+#ifndef EZLDA_SLOTS
+#define EZLDA_SLOTS 2
+#endif
+constexpr uint32_t kMaxSlots = EZLDA_SLOTS;  // slots per block when they fit (d.nslots: 1 for large K)
+constexpr uint32_t kExit = 0x80000000u;
+
+struct __align__(16) SlotCtl {
+  WordRec rec;
+  uint64_t mbar;
+  uint32_t v, r0, r1, ntok;
+  uint32_t cursor, done;
+  uint32_t sampled, hitM, runs, words, exact;
+  uint32_t state;  // block item number held by the slot (| kExit: no item left)
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+
+// per-slot dynamic shared memory: What'_f32 [Kpad] | QP f64 [Kpad] | hist u32 [Kpad]
+// (What'_f32 | QP is one bulk copy of a wrow record)
+__host__ __device__ __forceinline__ uint32_t slot_bytes(uint32_t K) { return 16u * ((K + 31u) / 32u) * 32u; }
+
+// Tail-word What' row staged by one warp when word-prep did not precompute it (v >= Vw):
+// the fp32 What' row and the sequential Q' prefix QP, the same expressions and order as
+// k_word_prep (QP doubles as the fp64 row while lane 0 runs the prefix in place).
+__device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, uint32_t K1, float* rowf, double* QP) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint32_t k0 = lane; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane
+    double x[8];
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+      const uint32_t k = k0 + 32u * i;
+      x[i] = (k < d.K) ? __ldg(d.what0 + k) : 0.0;
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i)
+      if (k0 + 32u * i < d.Kpad) QP[k0 + 32u * i] = x[i];
+  }
+  __syncwarp();
+  const uint32_t t = v - d.Vd;
+  const uint32_t* tr = cur.Wt + d.tofs[t];
+  const uint32_t n = cur.tnnz[t];
+  for (uint32_t e = lane; e < n; e += 32u) {
+    const uint32_t p = tr[e];
+    const uint32_t k = p >> 16;
+    QP[k] = ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
+  }
+  __syncwarp();
+  if (lane == 0) QP[K1] = 0.0;  // What' (Eq 6)
+  __syncwarp();
+  for (uint32_t k = lane; k < d.Kpad; k += 32u) rowf[k] = (float)QP[k];
+  __syncwarp();
+  if (lane == 0) {
+    double acc = 0.0;
+#pragma unroll 16
+    for (uint32_t k = 0; k < d.Kpad; ++k) {
+      acc = acc + QP[k];
+      QP[k] = acc;
+    }
+  }
+  __syncwarp();
+  for (uint32_t k = lane; k < d.Kpad; k += 32u) QP[k] = d.alpha * QP[k];
+  __syncwarp();
+}
+
+// Arm slot `sl` with block item k (one warp): claim the next global item, publish its
+// description, start the What' row transfer.  The slot's histogram is zero on entry.
+__device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char* sbase, uint32_t k, uint32_t n_items) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t i = 0;
+  if (lane == 0) i = (uint32_t)atomicAdd(&d.ctr->item_ctr, 1ull);
+  i = __shfl_sync(kFull, i, 0);
+  if (i >= n_items) {
+    if (lane == 0) st_release_s(&c.state, k | kExit);
+    return;
+  }
+  const uint32_t v = d.item_word[i];
+  float* rowf = reinterpret_cast<float*>(sbase);
+  double* QP = reinterpret_cast<double*>(sbase + 4u * d.Kpad);
+  const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&c.mbar);
+  if (lane < 6) reinterpret_cast<uint64_t*>(&c.rec)[lane] = reinterpret_cast<const uint64_t*>(d.rec + v)[lane];
+  if (lane == 0) {
+    c.v = v;
+    c.r0 = d.item_r0[i];
+    c.r1 = d.item_r1[i];
+    c.ntok = d.item_ntok[i];
+    c.cursor = 0;
+    c.done = 0;
+    c.sampled = 0;
+    c.hitM = 0;
+    c.runs = 0;
+    c.words = 0;
+    c.exact = 0;
+  }
+  if (v < d.Vw) {  // precomputed by word-prep
+    if (lane == 0) bulk_g2s((uint32_t)__cvta_generic_to_shared(rowf), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
+  } else {
+    __syncwarp();
+    stage_tail_row_warp(d, cur, v, c.rec.K[0], rowf, QP);
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
+  }
+  __syncwarp();
+  if (lane == 0) st_release_s(&c.state, k);
+}
+
+// Warp-level epilogue of a finished item: skipped tokens at K1, W row / n_k from the
+// histogram (dense: atomics; tail: ordered compaction into the packed row), histogram
+// re-zeroed for the slot's next item.
+__device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uint32_t* hist) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t v = c.v;
+  if (lane == 0) hist[c.rec.K[0]] += c.ntok - c.sampled;  // skipped tokens stay at K1
+  __syncwarp();
+  if (v < d.Vd) {
+    int32_t* Wrow = nxt.Wd + (size_t)v * d.K;
+    for (uint32_t k = lane; k < d.K; k += 32u) {
+      const uint32_t n = hist[k];
+      if (n) {
+        atomicAdd(&Wrow[k], (int32_t)n);
+        atomicAdd(&nxt.nk[k], (int32_t)n);
+        hist[k] = 0;
+      }
+    }
+  } else {
+    const uint32_t t = v - d.Vd;
+    uint32_t* out = nxt.Wt + d.tofs[t];
+    uint32_t nz = 0;
+    for (uint32_t base = 0; base < d.Kpad; base += 32u) {
+      const uint32_t k = base + lane;
+      const uint32_t n = hist[k];  // zero past K
+      const uint32_t m = __ballot_sync(kFull, n != 0);
+      if (n) {
+        out[nz + __popc(m & lanemask_lt())] = (k << 16) | n;
+        atomicAdd(&nxt.nk[k], (int32_t)n);
+        hist[k] = 0;
+      }
+      nz += __popc(m);
+    }
+    if (lane == 0) nxt.tnnz[t] = nz;
+  }
+  if (lane == 0) {
+    atomicAdd(&d.ctr->sampled, (unsigned long long)c.sampled);
+    atomicAdd(&d.ctr->skip_M, (unsigned long long)c.hitM);
+    atomicAdd(&d.ctr->active_runs, (unsigned long long)c.runs);
+    atomicAdd(&d.ctr->drow_words, (unsigned long long)c.words);
+    if (c.exact) atomicAdd(&d.ctr->exact, (unsigned long long)c.exact);
+  }
+  __syncwarp();
+}
+
+#ifndef EZLDA_SAMP_WARPS
+#define EZLDA_SAMP_WARPS 12
+#endif
+constexpr int kSampWarpsP = EZLDA_SAMP_WARPS;
+
+__host__ __device__ __forceinline__ uint32_t sampler_ws_offset(uint32_t K, uint32_t nslots) {
+  return (uint32_t)((sizeof(SlotCtl) * kMaxSlots + 15u) & ~15u) + nslots * slot_bytes(K);
+}
+
+#ifndef EZLDA_SAMP_MINB
+#define EZLDA_SAMP_MINB 2  // resident sampler blocks per SM the register allocation must allow
+#endif
+
+__global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter,
+                                                                  uint32_t n_items) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SlotCtl* ctl = reinterpret_cast<SlotCtl*>(smem);
+  unsigned char* slots = smem + ((sizeof(SlotCtl) * kMaxSlots + 15u) & ~15u);
+  const uint32_t sb = slot_bytes(d.K);
+  const uint32_t nsl = d.nslots;
+  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(smem + sampler_ws_offset(d.K, nsl));
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t nw = blockDim.x >> 5;
+  // prologue: barriers, zero histograms, warp 0 arms the first kSlots items
+  if (tid == 0) {
+    for (uint32_t sl = 0; sl < nsl; ++sl) {
+      const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&ctl[sl].mbar);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mb), "r"(1u) : "memory");
+      ctl[sl].state = 0xFFFFFFFFu;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (uint32_t sl = 0; sl < nsl; ++sl) {
+    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad);
+    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (uint32_t sl = 0; sl < nsl; ++sl) arm_slot(d, cur, ctl[sl], slots + sl * sb, sl, n_items);
+  WarpScratch& ws = s_ws[warp];
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t sl = k % nsl;
+    SlotCtl& c = ctl[sl];
+    uint32_t st = 0;
+    if (lane == 0) {
+      while (((st = ld_acquire_s(&c.state)) & ~kExit) != k) __nanosleep(32);
+    }
+    st = __shfl_sync(kFull, st, 0);
+    if (st & kExit) break;
+    mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
+    const double* QP = reinterpret_cast<const double*>(slots + sl * sb + 4u * d.Kpad);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad);
+    const WordRec rec = c.rec;
+    const uint32_t v = c.v, r0 = c.r0, r1 = c.r1;
+    const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(slots + sl * sb);
+    RunCounters rc{0, 0, 0, 0, 0};
+    uint32_t qn = 0;
+    bool exhausted = false;
+    while (true) {
+      // refill the queue with flagged runs (warp-uniform control flow throughout)
+      while (qn < 32 && !exhausted) {
+        uint32_t grp = 0;
+        if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
+        grp = __shfl_sync(kFull, grp, 0);
+        const uint32_t rb = r0 + grp * 32u;
+        if (rb >= r1) {
+          exhausted = true;
+          break;
+        }
+        const uint32_t r = rb + lane;
+        const bool act = (r < r1) && ((d.flags[r >> 5] >> (r & 31u)) & 1u);
+        const uint32_t m = __ballot_sync(kFull, act);
+        if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
+        qn += __popc(m);
+        __syncwarp();
+      }
+      if (qn == 0) break;
+      uint32_t nb;
+      switch (d.segw) {
+        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+      }
+      // drop the processed runs from the queue
+      const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
+      const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
+      __syncwarp();
+      if (lane + nb < qn) ws.q[lane] = keep0;
+      if (lane + 32u + nb < qn) ws.q[lane + 32u] = keep1;
+      qn -= nb;
+      __syncwarp();
+    }
+    const uint32_t smp = warp_sum(rc.sampled), hm = warp_sum(rc.hitM);
+    const uint32_t nr = warp_sum(rc.runs), nwd = warp_sum(rc.words), nex = warp_sum(rc.exact);
+    uint32_t last = 0;
+    if (lane == 0) {
+      if (nex) atomicAdd(&c.exact, nex);
+      if (smp) atomicAdd(&c.sampled, smp);
+      if (hm) atomicAdd(&c.hitM, hm);
+      if (nr) atomicAdd(&c.runs, nr);
+      if (nwd) atomicAdd(&c.words, nwd);
+      __threadfence_block();
+      last = (atomicAdd(&c.done, 1u) == nw - 1u);
+      if (last) __threadfence_block();
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      item_epilogue_warp(d, nxt, c, hist);
+      arm_slot(d, cur, c, slots + sl * sb, k + nsl, n_items);
+    }
+  }
+}
+
+// W / n_k of one item from its topic histogram, block-wide (dense rows: atomics, the item
+// may be one of several regions of the word; tail rows: ordered compaction).
 __device__ void item_epilogue(const Dev& d, const Buf& nxt, uint32_t v, const uint32_t* hist, uint32_t* s_wsum,
                               uint32_t* s_run) {
   const uint32_t tid = threadIdx.x;
@@ -777,120 +1139,6 @@ __device__ void item_epilogue(const Dev& d, const Buf& nxt, uint32_t v, const ui
       const uint32_t c = hist[k];
       if (c) atomicAdd(&nxt.nk[k], (int32_t)c);
     }
-  }
-}
-
-// byte offset of the per-warp scratch in the sampler's dynamic shared memory:
-// What' [Kpad] | QP [Kpad] | T [nch] | CP [nch + 1] | hist [Kpad] u32 | (16-aligned) scratch
-__host__ __device__ __forceinline__ uint32_t sampler_ws_offset(uint32_t K) {
-  const uint32_t nch = (K + 31) / 32;
-  const uint32_t b = 2u * nch * 32u * 8u + (2u * nch + 1u) * 8u + nch * 32u * 4u;
-  return (b + 15u) & ~15u;
-}
-
-#ifndef EZLDA_SAMP_MINB
-#define EZLDA_SAMP_MINB 3  // sampler blocks per SM the register allocation must allow
-#endif
-
-// shared memory of the sampler: What' row [Kpad] | CP [nch + 1] (one bulk copy, rs doubles)
-// | T [nch] | hist [Kpad] u32 | kSampWarps x WarpScratch
-__global__ void __launch_bounds__(kSampWarps * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* row = reinterpret_cast<double*>(smem);
-  double* QP = row + d.Kpad;
-  double* T = row + d.rs;
-  double* CP = T + d.nch;
-  uint32_t* hist = reinterpret_cast<uint32_t*>(CP + d.nch + 1);
-  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(smem + sampler_ws_offset(d.K));
-  __shared__ uint32_t s_cursor, s_wsum[32], s_run;
-  __shared__ uint32_t s_sampled, s_hitM, s_runs, s_words;
-  __shared__ __align__(8) uint64_t s_mbar;
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t item = blockIdx.x;
-  const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
-  const uint32_t ntok = d.item_ntok[item];
-  const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&s_mbar);
-  const bool dense = v < d.Vd;
-  if (dense && tid == 0) {  // TMA bulk copy of the precomputed What' row + QP
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar_s), "r"(1u) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    bulk_g2s((uint32_t)__cvta_generic_to_shared(row), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
-  }
-  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
-  if (tid == 0) { s_cursor = 0; s_sampled = 0; s_hitM = 0; s_runs = 0; s_words = 0; }
-  const WordRec rec = d.rec[v];
-  if (dense) {
-    __syncthreads();
-    mbar_wait(mbar_s, 0);
-  } else {
-    stage_row(d, cur, v, row);
-    if (tid == 0) row[rec.K[0]] = 0.0;  // What'
-    __syncthreads();
-    chunk_prefix(row, d.nch, T, CP);
-    q_prefix(row, d.nch, CP, d.alpha, QP);
-  }
-  RunCounters rc{0, 0, 0, 0};
-  {
-    WarpScratch& ws = s_ws[warp];
-    const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(row);
-    uint32_t qn = 0;
-    bool exhausted = false;
-    while (true) {
-      // refill the queue with flagged runs (warp-uniform control flow throughout)
-      while (qn < 32 && !exhausted) {
-        uint32_t grp = 0;
-        if (lane == 0) grp = atomicAdd(&s_cursor, 1u);
-        grp = __shfl_sync(kFull, grp, 0);
-        const uint32_t rb = r0 + grp * 32u;
-        if (rb >= r1) {
-          exhausted = true;
-          break;
-        }
-        const uint32_t r = rb + lane;
-        const bool act = (r < r1) && ((d.flags[r >> 5] >> (r & 31u)) & 1u);
-        const uint32_t m = __ballot_sync(kFull, act);
-        if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
-        qn += __popc(m);
-        __syncwarp();
-      }
-      if (qn == 0) break;
-      uint32_t nb;
-      switch (d.segw) {
-        case 16u: nb = sample_batch<16u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 32u: nb = sample_batch<32u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 64u: nb = sample_batch<64u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 128u: nb = sample_batch<128u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
-        default: nb = sample_batch<256u>(d, nxt, rec, row_s, QP, hist, ws, qn, iter, rc); break;
-      }
-      // drop the processed runs from the queue
-      const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
-      const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
-      __syncwarp();
-      if (lane + nb < qn) ws.q[lane] = keep0;
-      if (lane + 32u + nb < qn) ws.q[lane + 32u] = keep1;
-      qn -= nb;
-      __syncwarp();
-    }
-  }
-  {
-    const uint32_t smp = warp_sum(rc.sampled), hm = warp_sum(rc.hitM);
-    const uint32_t nr = warp_sum(rc.runs), nw = warp_sum(rc.words);
-    if (lane == 0) {
-      atomicAdd(&s_sampled, smp);
-      atomicAdd(&s_hitM, hm);
-      atomicAdd(&s_runs, nr);
-      atomicAdd(&s_words, nw);
-    }
-  }
-  __syncthreads();
-  if (tid == 0) hist[rec.K[0]] += ntok - s_sampled;  // skipped tokens stay at K1
-  __syncthreads();
-  item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
-  if (tid == 0) {
-    atomicAdd(&d.ctr->sampled, (unsigned long long)s_sampled);
-    atomicAdd(&d.ctr->skip_M, (unsigned long long)s_hitM);
-    atomicAdd(&d.ctr->active_runs, (unsigned long long)s_runs);
-    atomicAdd(&d.ctr->drow_words, (unsigned long long)s_words);
   }
 }
 
@@ -986,26 +1234,47 @@ __global__ void k_topics_from_input(const uint16_t* in, const uint32_t* perm, ui
 
 }  // namespace
 
-size_t word_prep_smem_bytes(uint32_t K) {
+size_t word_prep_smem_bytes(uint32_t K) { return (size_t)2 * ((K + 31) / 32) * 32 * 8; }  // row | QP
+size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32; }  // What' | QP
+uint32_t wrow_stride(uint32_t K) { return 3u * ((K + 31) / 32) * 16; }  // What'_f32 | QP (doubles)
 uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= 16 with K <= kSegCap segw
   uint32_t w = 16u;
   while (w * kSegCap < K) w <<= 1;
   return w;
 }
-size_t sampler_smem_bytes(uint32_t K) { return sampler_ws_offset(K) + sizeof(WarpScratch) * kSampWarps; }
+static size_t sampler_smem_bytes_n(uint32_t K, uint32_t nslots) {
+  return sampler_ws_offset(K, nslots) + sizeof(WarpScratch) * kSampWarpsP;
+}
+constexpr size_t kMaxSmem = 227u * 1024u;
+uint32_t sampler_slots(uint32_t K) {  // 0: does not fit
+  for (uint32_t n = kMaxSlots; n >= 1; --n)
+    if (sampler_smem_bytes_n(K, n) <= kMaxSmem) return n;
+  return 0;
+}
+size_t sampler_smem_bytes(uint32_t K) { return sampler_smem_bytes_n(K, std::max<uint32_t>(1u, sampler_slots(K))); }
 size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
+
+static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
+static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
 
 cudaError_t configure_kernels(uint32_t K) {
   cudaError_t e;
   const int wp = (int)word_prep_smem_bytes(K), sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = cudaFuncSetAttribute(k_word_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, wp))) return e;
-  if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, wp))) return e;
+  if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)llpt_smem_bytes(K)))) return e;
   if ((e = cudaFuncSetAttribute(k_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
+  {
+    int dev = 0, nsm = 0, nb = 0;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sampler, kSampWarpsP * 32, (size_t)sp))) return e;
+    if (nb < 1) return cudaErrorInvalidConfiguration;
+    g_sampler_grid = (uint32_t)(nsm * nb);
+  }
   if ((e = cudaFuncSetAttribute(k_wcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wcount_smem_bytes(K))))
     return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
@@ -1056,11 +1325,12 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
   if (count_only)
     k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
-    k_sampler<<<n_items, kSampWarps * 32, sampler_smem_bytes(d.K), s>>>(d, cur, nxt, iteration);
+    k_sampler<<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>(
+        d, cur, nxt, iteration, n_items);
 }
 
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {
-  if (n_items) k_llpt<<<n_items, kLlptWarps * 32, word_prep_smem_bytes(d.K), s>>>(d, cur, partial);
+  if (n_items) k_llpt<<<n_items, kLlptWarps * 32, llpt_smem_bytes(d.K), s>>>(d, cur, partial);
   k_sum<<<1, 256, 0, s>>>(partial, n_items, out);
 }
 

@@ -39,11 +39,16 @@ constexpr uint32_t kSegCap = EZLDA_SEGCAP;  // sampler: S' segments per warp bat
 
 struct Counters {  // device-side per-iteration counters
   unsigned long long skip_S, skip_M, sampled, active_runs, drow_words, d_nnz;
+  unsigned long long item_ctr;  // sampler work-list cursor (claimed items)
+  unsigned long long exact;     // tokens redrawn on the exact fp64 path
 };
 
 struct Dev {
   // sizes and parameters
   uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
+  uint32_t nslots;   // sampler item slots per block (sampler_slots(K))
+  uint32_t exact_all;  // 1: every sampled token takes the exact fp64 path (test/ablation knob)
+  uint32_t Vw;     // words v < Vw have their What' | QP row precomputed in wrow (Vd, or V if it fits)
   uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, 0x7FFF)
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
   uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
@@ -67,7 +72,7 @@ struct Dev {
   uint32_t* D;
   uint32_t* flags;
   WordRec* rec;
-  double* wrow;   // [Vd * rs] precomputed What' rows + chunk prefixes (dense words)
+  double* wrow;   // [Vw * rs] precomputed What' rows + Q' prefix tables (words v < Vw)
   double* den;    // [K] n_k + V beta
   double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
   Counters* ctr;
@@ -99,6 +104,7 @@ void launch_topics_to_input(const uint16_t* z, const uint32_t* perm, uint32_t N,
 void launch_topics_from_input(const uint16_t* in, const uint32_t* perm, uint32_t N, uint16_t* z, cudaStream_t s);
 
 size_t sampler_smem_bytes(uint32_t K);
+uint32_t sampler_slots(uint32_t K);  // pipelined item slots per sampler block (0: K too large)
 uint32_t wrow_stride(uint32_t K);
 uint32_t seg_width(uint32_t K);
 size_t word_prep_smem_bytes(uint32_t K);
