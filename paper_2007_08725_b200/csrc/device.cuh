@@ -79,23 +79,37 @@ __device__ __forceinline__ T warp_sum(T x) {
 // depth g; Alg MPTC): skip iff u < M / (M + S_est + Q').  Shared verbatim by the
 // doc pass and the sampler so both take the identical decision.
 // ---------------------------------------------------------------------------------
+// exact uint32 -> fp64 with the 2^52 trick (one DADD instead of an I2F.F64)
+__device__ __forceinline__ double u2d(uint32_t x) { return __hiloint2double(0x43300000, (int)x) - 0x1p52; }
+
 __device__ __forceinline__ double mpt_M(const WordRec& r, uint32_t C1, double alpha) {
-  return r.a[0] * ((double)C1 + alpha);
+  return r.a[0] * (u2d(C1) + alpha);
 }
 
-__device__ __forceinline__ double mpt_threshold(const WordRec& r, double M, uint32_t C1, uint32_t C2, uint32_t C3,
-                                                uint32_t L, uint32_t geff) {
+// S_est + ... denominator of the threshold: (M + S_est) + Q'
+__device__ __forceinline__ double mpt_den(const WordRec& r, double M, uint32_t C1, uint32_t C2, uint32_t C3,
+                                          uint32_t L, uint32_t geff) {
   double S_est;
   if (geff == 0) {
     S_est = 0.0;
   } else if (geff == 1) {
-    S_est = r.a[1] * (double)(L - C1);
+    S_est = r.a[1] * u2d(L - C1);
   } else if (geff == 2) {
-    S_est = r.a[1] * (double)C2 + r.a[2] * (double)(L - C1 - C2);
+    S_est = r.a[1] * u2d(C2) + r.a[2] * u2d(L - C1 - C2);
   } else {
-    S_est = (r.a[1] * (double)C2 + r.a[2] * (double)C3) + r.a[3] * (double)(L - C1 - C2 - C3);
+    S_est = (r.a[1] * u2d(C2) + r.a[2] * u2d(C3)) + r.a[3] * u2d(L - C1 - C2 - C3);
   }
-  return M / ((M + S_est) + r.Qp);
+  return (M + S_est) + r.Qp;
+}
+
+// The MPT decision u < thr with thr = M / den rounded as the oracle rounds it.  The
+// division is skipped when u den is clear of M by a relative 2^-50 (then u < M / den
+// and u < fl(M / den) agree); otherwise thr is formed exactly as written.
+__device__ __forceinline__ bool mpt_skip(double u, double M, double den) {
+  const double p = u * den;
+  if (p < M * (1.0 - 0x1p-50)) return true;
+  if (p > M * (1.0 + 0x1p-50)) return false;
+  return u < M / den;
 }
 
 }  // namespace ezl

@@ -112,21 +112,6 @@ __device__ __forceinline__ void top4_insert(Top4& t, double v, uint32_t k) {
   }
 }
 
-__device__ __forceinline__ void top4_warp_merge(Top4& t) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov[4];
-    uint32_t ok[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ov[i] = __shfl_xor_sync(kFull, t.v[i], o);
-      ok[i] = __shfl_xor_sync(kFull, t.k[i], o);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) top4_insert(t, ov[i], ok[i]);
-  }
-}
-
 // Block-wide ordered compaction: out[pos] = (k << 16) | hist[k] for every k < K with
 // hist[k] > 0, ascending k.  Returns nnz in all threads.
 __device__ uint32_t block_compact(const uint32_t* hist, uint32_t K, uint32_t* out, uint32_t* s_wsum,
@@ -168,70 +153,87 @@ __global__ void k_den(Dev d, Buf cur) {
   }
 }
 
-// H1: word-prep ("MPT generate").  One block per word.
-__global__ void __launch_bounds__(128) k_word_prep(Dev d, Buf cur) {
-  const uint32_t v = blockIdx.x;
-  if (d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard
+// H1: word-prep ("MPT generate", P:546 step 1).  One warp per word: stage the What row
+// in shared memory, top-4 (value desc, topic asc) by per-lane insertion + a 4-round warp
+// tournament, What' (K1 entry zeroed), then lane 0 runs the Q' prefix P_v(k) strictly
+// sequentially (the oracle's order: QP[k] = alpha P_v(k), Q' = alpha P_v(K-1) bit for bit)
+// while the other warps of the SM proceed with their words.
+constexpr uint32_t kWpWarps = 4;
+
+__global__ void __launch_bounds__(kWpWarps * 32) k_word_prep(Dev d, Buf cur) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* row = reinterpret_cast<double*>(smem);
-  double* QPs = row + d.Kpad;
-  __shared__ double s_v[4][4];
-  __shared__ uint32_t s_k[4][4];
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  stage_row(d, cur, v, row);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t v = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (v >= d.V || d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard (warp-uniform)
+  double* row = reinterpret_cast<double*>(smem) + (size_t)warp * d.Kpad;
+  if (v < d.Vd) {
+    const int32_t* w = cur.Wd + (size_t)v * d.K;
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) row[k] = (k < d.K) ? ((double)w[k] + d.beta) / d.den[k] : 0.0;
+  } else {
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) row[k] = (k < d.K) ? d.what0[k] : 0.0;
+    __syncwarp();
+    const uint32_t t = v - d.Vd;
+    const uint32_t* tr = cur.Wt + d.tofs[t];
+    const uint32_t n = cur.tnnz[t];
+    for (uint32_t e = lane; e < n; e += 32u) {
+      const uint32_t p = tr[e];
+      const uint32_t k = p >> 16;
+      row[k] = ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
+    }
+  }
+  __syncwarp();
+  // top-4: per-lane sorted lists over k = lane (mod 32), then 4 rounds of warp argmax
   Top4 t;
   top4_init(t);
-  for (uint32_t k = tid; k < d.K; k += blockDim.x) top4_insert(t, row[k], k);
-  top4_warp_merge(t);
-  if (lane == 0) {
+  for (uint32_t k = lane; k < d.K; k += 32u) top4_insert(t, row[k], k);
+  WordRec r;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { s_v[warp][i] = t.v[i]; s_k[warp][i] = t.k[i]; }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    Top4 f;
-    top4_init(f);
-    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w)
-      for (int i = 0; i < 4; ++i) top4_insert(f, s_v[w][i], s_k[w][i]);
-    WordRec r;
-    for (int i = 0; i < 4; ++i) {
-      const bool ok = f.v[i] >= 0.0;
-      r.a[i] = ok ? f.v[i] : 0.0;
-      r.K[i] = ok ? (uint16_t)f.k[i] : (uint16_t)0;
+  for (int i = 0; i < 4; ++i) {
+    double bv = t.v[0];
+    uint32_t bk = t.k[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, o);
+      const uint32_t ok = __shfl_xor_sync(kFull, bk, o);
+      if (better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
     }
-    row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
-    // Q' prefix P_v(k) = sum_{j <= k, j != K1} What[j], ascending and strictly sequential:
-    // the oracle's order, so QP[k] = alpha P_v(k) and Q' = alpha P_v(K-1) are its values bit
-    // for bit (padding past K adds +0.0)
-    // the loads of a 16-entry chunk are issued before the previous chunk's dependent adds
-    double acc = 0.0, x[16];
+    if (t.k[0] == bk) {  // the owner pops its head
+      t.v[0] = t.v[1]; t.k[0] = t.k[1];
+      t.v[1] = t.v[2]; t.k[1] = t.k[2];
+      t.v[2] = t.v[3]; t.k[2] = t.k[3];
+      t.v[3] = -1.0; t.k[3] = 0xFFFFFFFFu;
+    }
+    const bool ok = bv >= 0.0;
+    r.a[i] = ok ? bv : 0.0;
+    r.K[i] = ok ? (uint16_t)bk : (uint16_t)0;
+  }
+  if (lane == 0) row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
+  __syncwarp();
+  const bool out = v < d.Vw;
+  float* outf = reinterpret_cast<float*>(d.wrow + (size_t)v * d.rs);
+  double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
+  if (out)  // fp32 What'[v] for the sampler's bulk copy
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) outf[k] = (float)row[k];
+  if (lane == 0) {
+    // Q' prefix, strictly sequential; the next 8 entries are loaded before the dependent adds
+    double acc = 0.0, x[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = row[i];
-    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 16u) {  // Kpad is a multiple of 32
-      double xn[16];
+    for (int i = 0; i < 8; ++i) x[i] = row[i];
+    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 8u) {  // Kpad is a multiple of 32
+      double xn[8];
+      const uint32_t kn = (k0 + 8u < d.Kpad) ? k0 + 8u : k0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) xn[i] = (k0 + 16u < d.Kpad) ? row[k0 + 16u + i] : 0.0;
+      for (int i = 0; i < 8; ++i) xn[i] = row[kn + i];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < 8; ++i) {
         acc = acc + x[i];
-        QPs[k0 + i] = acc;
+        if (out) outq[k0 + i] = d.alpha * acc;
+        if (k0 + i == d.K - 1u) r.Qp = d.alpha * acc;
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) x[i] = xn[i];
+      for (int i = 0; i < 8; ++i) x[i] = xn[i];
     }
-    r.Qp = d.alpha * QPs[d.K - 1];
     d.rec[v] = r;
-  }
-  __syncthreads();
-  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) QPs[k] = d.alpha * QPs[k];
-  __syncthreads();
-  if (v < d.Vw) {  // fp32 What'[v] | QP for the sampler's bulk copy
-    float* outf = reinterpret_cast<float*>(d.wrow + (size_t)v * d.rs);
-    double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
-    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) {
-      outf[k] = (float)row[k];
-      outq[k] = QPs[k];
-    }
   }
 }
 
@@ -261,9 +263,9 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
     const uint32_t C2 = d.geff >= 2 ? C(r.K[1]) : 0u;
     const uint32_t C3 = d.geff >= 3 ? C(r.K[2]) : 0u;
     const double M = mpt_M(r, C1, d.alpha);
-    const double thr = mpt_threshold(r, M, C1, C2, C3, L, d.geff);
+    const double den = mpt_den(r, M, C1, C2, C3, L, d.geff);
     const double u = philox_u(d.seed, iter, d.token_base + j);
-    if (u < thr) {
+    if (mpt_skip(u, M, den)) {
       nxt.z[j] = r.K[0];
       ++n_skip;
     } else {
@@ -276,16 +278,20 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
 }
 
 // Warp tier, K <= 4096: one warp per doc with a private dense shared-memory histogram
-// (two 16-bit counters per word), C_j read straight from it, then an ordered
-// compaction over K that writes the packed D row and re-zeroes the counters.
+// (two 16-bit counters per word) and a topic bitmap, C_j read straight from the
+// histogram; the packed D row is emitted in topic order from the bitmap (each lane owns
+// 32-topic words: popcount prefix + set-bit walk, O(nnz + K/32) per doc) and both are
+// re-zeroed as they are read.
 template <bool kSkipTest>
 __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
                                                               uint32_t n_docs, uint32_t iter) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t hw = d.Kpad >> 1;  // counter words per warp
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * hw;
-  for (uint32_t i = lane; i < hw; i += 32) hist[i] = 0;
+  const uint32_t hw = d.Kpad >> 1;   // counter words per warp
+  const uint32_t bw = d.Kpad >> 5;   // bitmap words per warp
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * (hw + bw);
+  uint32_t* bmp = hist + hw;
+  for (uint32_t i = lane; i < hw + bw; i += 32) hist[i] = 0;
   __syncwarp();
   unsigned long long n_skip = 0, n_nnz = 0;
   for (uint32_t idx = blockIdx.x * kDocWarps + warp; idx < n_docs; idx += gridDim.x * kDocWarps) {
@@ -295,6 +301,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf
     for (uint32_t i = lane; i < L; i += 32) {
       const uint32_t k = cur.z[j0 + i];
       atomicAdd(&hist[k >> 1], 1u << ((k & 1u) << 4));
+      atomicOr(&bmp[k >> 5], 1u << (k & 31u));
     }
     __syncwarp();
     if (kSkipTest) {
@@ -302,24 +309,31 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf
                            [&](uint32_t k) { return (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu; }, n_skip);
       __syncwarp();
     }
-    uint32_t* Drow = d.D + d.ddb[doc];
+    uint32_t* Drow = d.D + d.ddb[doc] + kDHdr;
     uint32_t nnz = 0;
-    for (uint32_t base = 0; base < hw; base += 32) {
-      const uint32_t w = base + lane;
-      const uint32_t x = (w < hw) ? hist[w] : 0u;
-      const uint32_t lo = x & 0xFFFFu, hi = x >> 16;
-      const uint32_t mlo = __ballot_sync(kFull, lo != 0), mhi = __ballot_sync(kFull, hi != 0);
-      const uint32_t lt = lanemask_lt();
-      const uint32_t pos = nnz + __popc(mlo & lt) + __popc(mhi & lt);
-      if (lo) Drow[kDHdr + pos] = ((2u * w) << 16) | lo;
-      if (hi) Drow[kDHdr + pos + (lo != 0)] = ((2u * w + 1u) << 16) | hi;
-      if (x) hist[w] = 0;
-      nnz += __popc(mlo) + __popc(mhi);
+    for (uint32_t base = 0; base < bw; base += 32) {
+      const uint32_t wi = base + lane;
+      const uint32_t b = (wi < bw) ? bmp[wi] : 0u;
+      const uint32_t cnt = __popc(b);
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+      }
+      uint32_t pos = nnz + incl - cnt;
+      for (uint32_t m = b; m; m &= m - 1u) {
+        const uint32_t k = wi * 32u + (__ffs(m) - 1u);
+        Drow[pos++] = (k << 16) | ((hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu);
+      }
+      for (uint32_t m = b; m; m &= m - 1u) hist[(wi * 32u + (__ffs(m) - 1u)) >> 1] = 0u;
+      if (b) bmp[wi] = 0u;
+      nnz += __shfl_sync(kFull, incl, 31);
     }
-    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[kDHdr + p] = 0u;  // pad to 8
+    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[p] = 0u;  // pad to 8
     if (lane == 0) {
-      Drow[0] = (L << 16) | nnz;
-      Drow[1] = j0;
+      Drow[-(int)kDHdr] = (L << 16) | nnz;
+      Drow[1 - (int)kDHdr] = j0;
     }
     n_nnz += nnz;
     __syncwarp();
@@ -1234,7 +1248,11 @@ __global__ void k_topics_from_input(const uint16_t* in, const uint32_t* perm, ui
 
 }  // namespace
 
-size_t word_prep_smem_bytes(uint32_t K) { return (size_t)2 * ((K + 31) / 32) * 32 * 8; }  // row | QP
+static uint32_t word_prep_warps(uint32_t K) {  // words (warps) per block: their rows must fit in smem
+  const size_t row = (size_t)((K + 31) / 32) * 32 * 8;
+  return (uint32_t)std::max<size_t>(1, std::min<size_t>(kWpWarps, (227u * 1024u) / row));
+}
+size_t word_prep_smem_bytes(uint32_t K) { return (size_t)word_prep_warps(K) * ((K + 31) / 32) * 32 * 8; }
 size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
@@ -1280,7 +1298,7 @@ cudaError_t configure_kernels(uint32_t K) {
   if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if (K <= 4096) {
-    const int dh = kDocWarps * (int)(((K + 31) / 32) * 16) * 4;
+    const int dh = kDocWarps * (int)(((K + 31) / 32) * 17) * 4;
     if ((e = cudaFuncSetAttribute(k_doc_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
     if ((e = cudaFuncSetAttribute(k_doc_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
   }
@@ -1292,7 +1310,8 @@ void launch_den(const Dev& d, const Buf& cur, cudaStream_t s) {
 }
 
 void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s) {
-  k_word_prep<<<d.V, 128, word_prep_smem_bytes(d.K), s>>>(d, cur);
+  const uint32_t wpw = word_prep_warps(d.K);
+  k_word_prep<<<(d.V + wpw - 1) / wpw, wpw * 32, word_prep_smem_bytes(d.K), s>>>(d, cur);
 }
 
 void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_t* docs_w, uint32_t n_w,
@@ -1305,7 +1324,7 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
   }
   if (n_w && d.K <= 4096) {
     const uint32_t grid = std::min<uint32_t>((n_w + kDocWarps - 1) / kDocWarps, 148u * 16u);
-    const size_t smem = (size_t)kDocWarps * (d.Kpad / 2) * 4;
+    const size_t smem = (size_t)kDocWarps * (d.Kpad / 2 + d.Kpad / 32) * 4;
     if (skip_test)
       k_doc_hist<true><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
     else
