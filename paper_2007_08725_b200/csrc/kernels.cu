@@ -524,18 +524,6 @@ __device__ __forceinline__ double entry_fma(uint32_t w, uint32_t row_s, double a
   return __fma_rn(c, f32bits_to_f64(lds_u32(row_s + ((w >> 16) << 2))), acc);
 }
 
-__device__ __forceinline__ double sector_sum(double acc, const uint4& a, const uint4& b, uint32_t row_s) {
-  acc = entry_fma(a.x, row_s, acc);
-  acc = entry_fma(a.y, row_s, acc);
-  acc = entry_fma(a.z, row_s, acc);
-  acc = entry_fma(a.w, row_s, acc);
-  acc = entry_fma(b.x, row_s, acc);
-  acc = entry_fma(b.y, row_s, acc);
-  acc = entry_fma(b.z, row_s, acc);
-  acc = entry_fma(b.w, row_s, acc);
-  return acc;
-}
-
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
@@ -707,9 +695,15 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
         if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
         if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
-        acc = sector_sum(acc, qa, qb, row_s);
+        acc = entry_fma(qa.x, row_s, acc); acc = entry_fma(qa.y, row_s, acc);
+        acc = entry_fma(qa.z, row_s, acc); acc = entry_fma(qa.w, row_s, acc);
+        acc = entry_fma(qb.x, row_s, acc); acc = entry_fma(qb.y, row_s, acc);
+        acc = entry_fma(qb.z, row_s, acc); acc = entry_fma(qb.w, row_s, acc);
         if (kSec) acc8 = acc;
-        acc = sector_sum(acc, qc, qd, row_s);
+        acc = entry_fma(qc.x, row_s, acc); acc = entry_fma(qc.y, row_s, acc);
+        acc = entry_fma(qc.z, row_s, acc); acc = entry_fma(qc.w, row_s, acc);
+        acc = entry_fma(qd.x, row_s, acc); acc = entry_fma(qd.y, row_s, acc);
+        acc = entry_fma(qd.z, row_s, acc); acc = entry_fma(qd.w, row_s, acc);
       }
     }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
@@ -747,26 +741,30 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
     const uint32_t i = B0 + lane;
-    if (i >= ntb) continue;
     const uint32_t j = s_j0 + (i - s_tofs);
-    const uint32_t zm = nxt.z[j];
     const uint32_t* E = d.D + s_ebase;
-    uint32_t C1;
-    if (d.zmark) {
-      if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
-      C1 = zm & 0x7FFFu;
-      if (C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
-    } else {
-      if (zm != kUnsampled) continue;
-      C1 = row_count(E, s_nnz, K1);
+    bool act = i < ntb;
+    uint32_t C1 = 0;
+    if (act) {
+      const uint32_t zm = nxt.z[j];
+      if (d.zmark) {
+        act = (zm & 0x8000u) != 0;  // else skipped by the MPT test (z^i = K1 < 0x8000)
+        C1 = zm & 0x7FFFu;
+        if (act && C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
+      } else {
+        act = zm == kUnsampled;
+        if (act) C1 = row_count(E, s_nnz, K1);
+      }
     }
+    if (!__any_sync(kFull, act)) continue;
     constexpr uint32_t kCk = kSec ? 2u : 1u;  // checkpoints per segment
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
-    const double Sp = nck ? ws.P[c0 + nck - 1u] : 0.0;
+    const double Sp = (act && nck) ? ws.P[c0 + nck - 1u] : 0.0;
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
-    const double u = philox_u(d.seed, iter, d.token_base + j);
+    const double u = act ? philox_u(d.seed, iter, d.token_base + j) : 0.0;
     const double x = u * Z;
+    if (!act) continue;
     // certification margin: every prefix P~ of the fast path satisfies |P~ - P| <= (2^-24 +
     // (nnz + 48) 2^-53) S' (fp32 rounding of What', one fp64 rounding per entry / scan level
     // / carry / walk step); x and y inherit it at most twice; 4e-15 Z covers the fp64
