@@ -210,10 +210,19 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep(Dev d, Buf cur) {
   if (lane == 0) row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
   __syncwarp();
   const bool out = v < d.Vw;
-  float* outf = reinterpret_cast<float*>(d.wrow + (size_t)v * d.rs);
+  uint32_t* outm = reinterpret_cast<uint32_t*>(d.wrow + (size_t)v * d.rs);
   double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
-  if (out)  // fp32 What'[v] for the sampler's bulk copy
-    for (uint32_t k = lane; k < d.Kpad; k += 32u) outf[k] = (float)row[k];
+  if (out) {  // fixed-point What'[v] (m = rint(What' 2^s), s from max What' = a2) + scale
+    int e = 0;
+    frexp(r.a[1], &e);
+    const int sh = 32 - e;  // max What' 2^sh in [2^31, 2^32)
+    for (uint32_t k = lane; k < d.Kpad; k += 32u)
+      outm[k] = __double2uint_rn(fmin(ldexp(row[k], sh), 4294967295.0));
+    if (lane == 0) {
+      outq[d.Kpad] = ldexp(1.0, -sh);
+      outq[d.Kpad + 1u] = ldexp(1.0, sh);
+    }
+  }
   if (lane == 0) {
     // Q' prefix, strictly sequential; the next 8 entries are loaded before the dependent adds
     double acc = 0.0, x[8];
@@ -492,7 +501,7 @@ struct RunCounters {
 constexpr int kQueue = 64;  // one batch + one refill group
 
 struct __align__(16) WarpScratch {
-  double P[2 * kSegCap];  // prefix checkpoints of the batch's runs, flattened (see sample_batch)
+  unsigned long long P[2 * kSegCap];  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
   uint32_t q[kQueue];     // queue of flagged runs
 };
 
@@ -509,19 +518,24 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-// fp32 bit pattern -> the same value in fp64, exact for positive normal floats (three
-// integer ops instead of an F2F conversion); +0.0f maps to 2^-127, which the certification
-// margin of sample_batch absorbs
-__device__ __forceinline__ double f32bits_to_f64(uint32_t f) {
-  return __hiloint2double((int)((f >> 3) + 0x38000000u), (int)(f << 29));
+// acc + D[d][k] m_v[k] for one packed entry (topic << 16 | count): m_v is the word's
+// fixed-point What' row (What' ~ m 2^-s), the product and the sum are exact 64-bit integers
+// (IMAD.WIDE.U32); padding (0) adds 0.
+__device__ __forceinline__ unsigned long long entry_mac(uint32_t w, uint32_t row_s, unsigned long long acc) {
+  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + ((w >> 16) << 2));
 }
 
-// acc + D[d][k] What'_f32[v][k] for one packed entry (topic << 16 | count): the product is
-// exact in fp64 (16 x 24 bits), one rounding per entry (DFMA); the count converts exactly
-// with the 2^52 trick; padding (0) adds +0.
-__device__ __forceinline__ double entry_fma(uint32_t w, uint32_t row_s, double acc) {
-  const double c = __hiloint2double(0x43300000, (int)(w & 0xFFFFu)) - 0x1p52;
-  return __fma_rn(c, f32bits_to_f64(lds_u32(row_s + ((w >> 16) << 2))), acc);
+__device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc, const uint4& a, const uint4& b,
+                                                         uint32_t row_s) {
+  acc = entry_mac(a.x, row_s, acc);
+  acc = entry_mac(a.y, row_s, acc);
+  acc = entry_mac(a.z, row_s, acc);
+  acc = entry_mac(a.w, row_s, acc);
+  acc = entry_mac(b.x, row_s, acc);
+  acc = entry_mac(b.y, row_s, acc);
+  acc = entry_mac(b.z, row_s, acc);
+  acc = entry_mac(b.w, row_s, acc);
+  return acc;
 }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
@@ -627,19 +641,22 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 // is redrawn by exact_draw.  Either way the topic equals the oracle's fp64 decision.
 template <uint32_t kSegW>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
-                                                 uint32_t v, uint32_t row_s, const double* QP, uint32_t* hist,
-                                                 WarpScratch& ws, uint32_t qn, uint32_t iter, RunCounters& rc) {
+                                                 uint32_t v, uint32_t row_s, const double* QP, double inv_s,
+                                                 double two_s, uint32_t* hist, WarpScratch& ws, uint32_t qn,
+                                                 uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
   // ---- A: lane per run: run table + header, segment admission
   const uint32_t nc = min(qn, 32u);
-  uint32_t j0 = 0, ebase = 0, len = 0, nnz = 0, nseg = 0;
+  uint32_t j0 = 0, ebase = 0, len = 0, nnz = 0, nseg = 0, Ld = 0;
   if (lane < nc) {
     const uint32_t r = ws.q[lane];
     j0 = d.run_j0[r];
     const uint32_t dbase = d.run_dbase[r];
     len = d.run_len[r];
-    nnz = d.D[dbase] & 0xFFFFu;
+    const uint32_t hdr = d.D[dbase];
+    nnz = hdr & 0xFFFFu;
+    Ld = hdr >> 16;
     ebase = dbase + kDHdr;
     nseg = (nnz + kSegW - 1u) / kSegW;
   }
@@ -673,13 +690,13 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     return nbefore + __popc(bits & (0xFFFFFFFFu >> (31u - lane))) - 1u;
   };
   // ---- B: lane per segment (kSegW entries, 16 = two 32-byte sectors); consecutive lanes
-  //      read consecutive sectors of a row.  The segment sums are combined into the run
-  //      prefixes by a segmented warp scan (carry across rounds).  Checkpoints: kSec
-  //      (kSegW = 16) keeps two per segment, P[2g] = P(before g) + (first sector) and
-  //      P[2g+1] = P(end of g), so a descent walks at most one sector; otherwise P[g] = P(end
-  //      of g).  S' = the run's last checkpoint.
+  //      read consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the
+  //      word's fixed-point What' row), combined by a segmented warp scan (+ carry across
+  //      rounds).  Checkpoints: kSec (kSegW = 16) keeps two per segment, P[2g] = P(before g)
+  //      + (first sector) and P[2g+1] = P(end of g), so a descent walks at most one sector;
+  //      otherwise P[g] = P(end of g).  S' = the run's last checkpoint.
   constexpr bool kSec = kSegW == 16u;
-  double carry = 0.0;
+  unsigned long long carry = 0ull;
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
     const uint32_t g = B0 + lane;
     const uint32_t slot = slot_of(B0, soff);
@@ -688,36 +705,30 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
     const uint32_t e0 = (g - s_soff) * kSegW;
     const uint32_t* p = d.D + s_ebase + e0;
-    double acc = 0.0, acc8 = 0.0;
+    unsigned long long acc = 0ull, acc8 = 0ull;
     if (g < T) {
 #pragma unroll
       for (uint32_t b = 0; b < kSegW; b += 16u) {
         uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
         if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
         if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
-        acc = entry_fma(qa.x, row_s, acc); acc = entry_fma(qa.y, row_s, acc);
-        acc = entry_fma(qa.z, row_s, acc); acc = entry_fma(qa.w, row_s, acc);
-        acc = entry_fma(qb.x, row_s, acc); acc = entry_fma(qb.y, row_s, acc);
-        acc = entry_fma(qb.z, row_s, acc); acc = entry_fma(qb.w, row_s, acc);
+        acc = sector_mac(acc, qa, qb, row_s);
         if (kSec) acc8 = acc;
-        acc = entry_fma(qc.x, row_s, acc); acc = entry_fma(qc.y, row_s, acc);
-        acc = entry_fma(qc.z, row_s, acc); acc = entry_fma(qc.w, row_s, acc);
-        acc = entry_fma(qd.x, row_s, acc); acc = entry_fma(qd.y, row_s, acc);
-        acc = entry_fma(qd.z, row_s, acc); acc = entry_fma(qd.w, row_s, acc);
+        acc = sector_mac(acc, qc, qd, row_s);
       }
     }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(kFull, acc, o);
-      if (lane >= rs + (uint32_t)o) acc = y + acc;
+      const unsigned long long y = __shfl_up_sync(kFull, acc, o);
+      if (lane >= rs + (uint32_t)o) acc += y;
     }
     const bool cont = s_soff < B0;  // the run started in an earlier round
-    if (cont) acc = carry + acc;
+    if (cont) acc += carry;
     if (kSec) {
-      double excl = __shfl_up_sync(kFull, acc, 1);
-      if (lane == rs) excl = cont ? carry : 0.0;
+      unsigned long long excl = __shfl_up_sync(kFull, acc, 1);
+      if (lane == rs) excl = cont ? carry : 0ull;
       if (g < T) {
         ws.P[2u * g] = excl + acc8;
         ws.P[2u * g + 1u] = acc;
@@ -740,36 +751,34 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t s_nseg = __shfl_sync(kFull, nseg, slot);
     const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
+    const uint32_t s_L = __shfl_sync(kFull, Ld, slot);
     const uint32_t i = B0 + lane;
+    if (i >= ntb) continue;
     const uint32_t j = s_j0 + (i - s_tofs);
     const uint32_t* E = d.D + s_ebase;
-    bool act = i < ntb;
-    uint32_t C1 = 0;
-    if (act) {
-      const uint32_t zm = nxt.z[j];
-      if (d.zmark) {
-        act = (zm & 0x8000u) != 0;  // else skipped by the MPT test (z^i = K1 < 0x8000)
-        C1 = zm & 0x7FFFu;
-        if (act && C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
-      } else {
-        act = zm == kUnsampled;
-        if (act) C1 = row_count(E, s_nnz, K1);
-      }
+    const uint32_t zm = nxt.z[j];
+    uint32_t C1;
+    if (d.zmark) {
+      if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
+      C1 = zm & 0x7FFFu;
+      if (C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
+    } else {
+      if (zm != kUnsampled) continue;
+      C1 = row_count(E, s_nnz, K1);
     }
-    if (!__any_sync(kFull, act)) continue;
     constexpr uint32_t kCk = kSec ? 2u : 1u;  // checkpoints per segment
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
-    const double Sp = (act && nck) ? ws.P[c0 + nck - 1u] : 0.0;
+    const unsigned long long Spi = nck ? ws.P[c0 + nck - 1u] : 0ull;
+    const double Sp = (double)Spi * inv_s;  // exact: Spi < 2^48
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
-    const double u = act ? philox_u(d.seed, iter, d.token_base + j) : 0.0;
+    const double u = philox_u(d.seed, iter, d.token_base + j);
     const double x = u * Z;
-    if (!act) continue;
-    // certification margin: every prefix P~ of the fast path satisfies |P~ - P| <= (2^-24 +
-    // (nnz + 48) 2^-53) S' (fp32 rounding of What', one fp64 rounding per entry / scan level
-    // / carry / walk step); x and y inherit it at most twice; 4e-15 Z covers the fp64
-    // roundings of M, Z, x and the oracle's own sums
-    const double mg = 2.0 * (5.9604644775390625e-8 + (double)(s_nnz + 48u) * 1.1102230246251565e-16) * Sp + 4e-15 * Z;
+    // certification margin: m_v[k] 2^-s is within 2^-s of What'[v][k], so every fixed-point
+    // prefix is within L_d 2^-s of the exact real prefix (the integer sums themselves are
+    // exact); x and y inherit it at most twice; 4e-15 Z covers the fp64 roundings of M, Z,
+    // x and of the oracle's own sums
+    const double mg = 2.0 * (double)s_L * inv_s + 4e-15 * Z;
     uint32_t topic = 0xFFFFFFFFu;
     bool hit = false;
     if (!d.exact_all && fabs(x - M) > mg && fabs(x - (M + Sp)) > mg) {
@@ -777,48 +786,48 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         topic = K1;  // second chance: u < M / (M + S' + Q')
         hit = true;
       } else if (x < M + Sp) {
-        // S' branch: first checkpoint with P > y, then the walk from the previous one
+        // S' branch: first checkpoint with P > y, then the walk from the previous one, all
+        // in exact integers against Yf = floor(y 2^s)  (P > y  <=>  P > Yf for integer P)
         const double y = x - M;
+        const unsigned long long Yf = (unsigned long long)(y * two_s);
         uint32_t a = c0, b = c0 + nck - 1u;
         while (a < b) {
           const uint32_t mid = (a + b) >> 1;
-          if (ws.P[mid] > y) b = mid; else a = mid + 1u;
+          if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
         }
-        const double base = (a > c0) ? ws.P[a - 1u] : 0.0;
-        double pb = base;  // prefix before the candidate entry
+        const unsigned long long base = (a > c0) ? ws.P[a - 1u] : 0ull;
+        unsigned long long pb = base, pa = base;  // prefixes before / after the candidate
         if (kSec) {  // one sector (8 entries; zero padding past nnz) from registers
           uint4 qa, qb;
           ldg256(E + (a - c0) * 8u, qa, qb);
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-          double acc = 0.0;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t w = wv[e];
             if (topic == 0xFFFFFFFFu && w != 0u) {
-              acc = entry_fma(w, row_s, acc);
-              const double pa = base + acc;
-              if ((w >> 16) != K1 && pa > y) {
-                topic = (pa - y > mg && y - pb > mg) ? (w >> 16) : 0xFFFFFFFEu;
-              }
-              pb = pa;
+              const unsigned long long q = entry_mac(w, row_s, pa);
+              if ((w >> 16) != K1 && q > Yf) topic = w >> 16;
+              else pb = q;
+              pa = q;
             }
           }
         } else {
           const uint32_t e0 = (a - c0) * kSegW;
           const uint32_t e1 = min(e0 + kSegW, s_nnz);
-          double acc = 0.0;
           for (uint32_t e = e0; e < e1; ++e) {
             const uint32_t w = __ldg(E + e);
-            acc = entry_fma(w, row_s, acc);
-            const double pa = base + acc;
-            if ((w >> 16) != K1 && pa > y) {
-              topic = (pa - y > mg && y - pb > mg) ? (w >> 16) : 0xFFFFFFFEu;
+            const unsigned long long q = entry_mac(w, row_s, pa);
+            pa = q;
+            if ((w >> 16) != K1 && q > Yf) {
+              topic = w >> 16;
               break;
             }
-            pb = pa;
+            pb = q;
           }
         }
-        if (topic == 0xFFFFFFFEu) topic = 0xFFFFFFFFu;  // uncertified: exact redraw
+        // certify: the candidate's interval [pb, pa) holds y with margin on both sides
+        if (topic != 0xFFFFFFFFu && !((double)pa * inv_s - y > mg && y - (double)pb * inv_s > mg))
+          topic = 0xFFFFFFFFu;  // uncertified: exact redraw
       } else {
         // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
         // is flat across K1 and holds the oracle's values)
@@ -882,15 +891,17 @@ __device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
                : "memory");
 }
 
-// per-slot dynamic shared memory: What'_f32 [Kpad] | QP f64 [Kpad] | hist u32 [Kpad]
-// (What'_f32 | QP is one bulk copy of a wrow record)
-__host__ __device__ __forceinline__ uint32_t slot_bytes(uint32_t K) { return 16u * ((K + 31u) / 32u) * 32u; }
+// per-slot dynamic shared memory: m u32 [Kpad] | QP f64 [Kpad] | (2^-s, 2^s) f64 | hist u32 [Kpad]
+// (m | QP | scale is one bulk copy of a wrow record)
+__host__ __device__ __forceinline__ uint32_t slot_bytes(uint32_t K) { return 16u * ((K + 31u) / 32u) * 32u + 16u; }
 
-// Tail-word What' row staged by one warp when word-prep did not precompute it (v >= Vw):
-// the fp32 What' row and the sequential Q' prefix QP, the same expressions and order as
-// k_word_prep (QP doubles as the fp64 row while lane 0 runs the prefix in place).
-__device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, uint32_t K1, float* rowf, double* QP) {
+// Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
+// fixed-point What' row + scale and the sequential Q' prefix QP, the same expressions and
+// order as k_word_prep (QP doubles as the fp64 row while lane 0 runs the prefix in place).
+__device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, uint32_t* m,
+                                    double* QP) {
   const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t K1 = rec.K[0];
   for (uint32_t k0 = lane; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane
     double x[8];
 #pragma unroll
@@ -914,7 +925,14 @@ __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, ui
   __syncwarp();
   if (lane == 0) QP[K1] = 0.0;  // What' (Eq 6)
   __syncwarp();
-  for (uint32_t k = lane; k < d.Kpad; k += 32u) rowf[k] = (float)QP[k];
+  int e = 0;
+  frexp(rec.a[1], &e);
+  const int sh = 32 - e;
+  for (uint32_t k = lane; k < d.Kpad; k += 32u) m[k] = __double2uint_rn(fmin(ldexp(QP[k], sh), 4294967295.0));
+  if (lane == 0) {
+    QP[d.Kpad] = ldexp(1.0, -sh);
+    QP[d.Kpad + 1u] = ldexp(1.0, sh);
+  }
   __syncwarp();
   if (lane == 0) {
     double acc = 0.0;
@@ -941,7 +959,7 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
     return;
   }
   const uint32_t v = d.item_word[i];
-  float* rowf = reinterpret_cast<float*>(sbase);
+  uint32_t* mrow = reinterpret_cast<uint32_t*>(sbase);
   double* QP = reinterpret_cast<double*>(sbase + 4u * d.Kpad);
   const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&c.mbar);
   if (lane < 6) reinterpret_cast<uint64_t*>(&c.rec)[lane] = reinterpret_cast<const uint64_t*>(d.rec + v)[lane];
@@ -959,10 +977,10 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
     c.exact = 0;
   }
   if (v < d.Vw) {  // precomputed by word-prep
-    if (lane == 0) bulk_g2s((uint32_t)__cvta_generic_to_shared(rowf), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
+    if (lane == 0) bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
   } else {
     __syncwarp();
-    stage_tail_row_warp(d, cur, v, c.rec.K[0], rowf, QP);
+    stage_tail_row_warp(d, cur, v, c.rec, mrow, QP);
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
   }
   __syncwarp();
@@ -1047,7 +1065,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (uint32_t sl = 0; sl < nsl; ++sl) {
-    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad + 16u);
     for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
   }
   __syncthreads();
@@ -1065,7 +1083,8 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     if (st & kExit) break;
     mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
     const double* QP = reinterpret_cast<const double*>(slots + sl * sb + 4u * d.Kpad);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad);
+    const double inv_s = QP[d.Kpad], two_s = QP[d.Kpad + 1u];  // fixed-point scale of m
+    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad + 16u);
     const WordRec rec = c.rec;
     const uint32_t v = c.v, r0 = c.r0, r1 = c.r1;
     const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(slots + sl * sb);
@@ -1093,11 +1112,11 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
       if (qn == 0) break;
       uint32_t nb;
       switch (d.segw) {
-        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
-        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
-        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, QP, hist, ws, qn, iter, rc); break;
+        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
+        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
+        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
+        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
+        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
       }
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
@@ -1255,7 +1274,7 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-uint32_t wrow_stride(uint32_t K) { return 3u * ((K + 31) / 32) * 16; }  // What'_f32 | QP (doubles)
+uint32_t wrow_stride(uint32_t K) { return 3u * ((K + 31) / 32) * 16 + 2u; }  // m u32 | QP | scale (doubles)
 uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= 16 with K <= kSegCap segw
   uint32_t w = 16u;
   while (w * kSegCap < K) w <<= 1;
