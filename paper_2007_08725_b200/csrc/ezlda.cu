@@ -959,7 +959,7 @@ ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W
         const uint32_t p = Dh[base + ezl::kDHdr + e];
         if (fill) {
           if (nnz >= D->nnz) return h->fail(EZLDA_E_INVALID, "D csr capacity too small");
-          D->col[nnz] = (uint16_t)(p >> 16);
+          D->col[nnz] = (uint16_t)ezl::d_topic(p);
           D->val[nnz] = (int32_t)(p & 0xFFFFu);
         }
         ++nnz;

@@ -112,10 +112,10 @@ __device__ __forceinline__ void top4_insert(Top4& t, double v, uint32_t k) {
   }
 }
 
-// Block-wide ordered compaction: out[pos] = (k << 16) | hist[k] for every k < K with
+// Block-wide ordered compaction: out[pos] = (k << shift) | hist[k] for every k < K with
 // hist[k] > 0, ascending k.  Returns nnz in all threads.
 __device__ uint32_t block_compact(const uint32_t* hist, uint32_t K, uint32_t* out, uint32_t* s_wsum,
-                                  uint32_t* s_run) {
+                                  uint32_t* s_run, uint32_t shift) {
   const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5, nw = nt >> 5;
   if (tid == 0) *s_run = 0;
   __syncthreads();
@@ -129,7 +129,7 @@ __device__ uint32_t block_compact(const uint32_t* hist, uint32_t K, uint32_t* ou
     uint32_t before = 0;
     for (uint32_t w = 0; w < warp; ++w) before += s_wsum[w];
     const uint32_t pos = *s_run + before + __popc(m & lanemask_lt());
-    if (f) out[pos] = (k << 16) | c;
+    if (f) out[pos] = (k << shift) | c;
     __syncthreads();
     if (tid == 0) {
       uint32_t tot = 0;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf
       uint32_t pos = nnz + incl - cnt;
       for (uint32_t m = b; m; m &= m - 1u) {
         const uint32_t k = wi * 32u + (__ffs(m) - 1u);
-        Drow[pos++] = (k << 16) | ((hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu);
+        Drow[pos++] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu);
       }
       for (uint32_t m = b; m; m &= m - 1u) hist[(wi * 32u + (__ffs(m) - 1u)) >> 1] = 0u;
       if (b) bmp[wi] = 0u;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf
     const uint32_t s1 = (p + 1 < nnz) ? (uint32_t)ust[p + 1] : L;
     const uint32_t cnt = s1 - s0;
     ucnt[p] = (uint16_t)cnt;
-    Drow[kDHdr + p] = ((uint32_t)ukey[p] << 16) | cnt;
+    Drow[kDHdr + p] = d_entry(ukey[p], cnt);
   }
   for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[kDHdr + p] = 0u;  // pad to 8
   if (lane == 0) {
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
   for (uint32_t i = tid; i < L; i += nt) atomicAdd(&hist[cur.z[j0 + i]], 1u);
   __syncthreads();
   uint32_t* Drow = d.D + dbase;
-  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run);
+  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run, kDT);
   for (uint32_t p = nnz + tid; p < ((nnz + 7u) & ~7u); p += nt) Drow[kDHdr + p] = 0u;  // pad to 8
   if (tid == 0) {
     Drow[0] = (L << 16) | nnz;
@@ -518,11 +518,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-// acc + D[d][k] m_v[k] for one packed entry (topic << 16 | count): m_v is the word's
+// acc + D[d][k] m_v[k] for one packed entry (topic << 18 | count): m_v is the word's
 // fixed-point What' row (What' ~ m 2^-s), the product and the sum are exact 64-bit integers
 // (IMAD.WIDE.U32); padding (0) adds 0.
 __device__ __forceinline__ unsigned long long entry_mac(uint32_t w, uint32_t row_s, unsigned long long acc) {
-  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + ((w >> 16) << 2));
+  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + (w >> 16));  // w >> 16 = 4 topic
 }
 
 __device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc, const uint4& a, const uint4& b,
@@ -558,17 +558,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar_s, uint32_t parity) {
 
 // C1 = D[d][K1] by binary search in the sorted packed row (fallback path: K > 32768 or
 // C1 >= 0x7FFF, where the doc pass cannot carry C1 in the z^i marker).
-__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
+template <uint32_t kShift>
+__device__ __forceinline__ uint32_t packed_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
   uint32_t lo = 0, hi = nnz;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if ((__ldg(E + mid) >> 16) < k) lo = mid + 1u; else hi = mid;
+    if ((__ldg(E + mid) >> kShift) < k) lo = mid + 1u; else hi = mid;
   }
   if (lo < nnz) {
     const uint32_t w = __ldg(E + lo);
-    if ((w >> 16) == k) return w & 0xFFFFu;
+    if ((w >> kShift) == k) return w & 0xFFFFu;
   }
   return 0u;
+}
+// D[d][k] of a packed D row / W[v][k] of a packed tail row
+__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
+  return packed_count<kDT>(E, nnz, k);
+}
+__device__ __forceinline__ uint32_t tail_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
+  return packed_count<16u>(E, nnz, k);
 }
 
 // What[v][k] in fp64 exactly as word-prep / the oracle form it: (W[v][k] + beta) / den_k.
@@ -579,7 +587,7 @@ __device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint3
   } else {
     const uint32_t t = v - d.Vd;
     const uint32_t* tr = cur.Wt + d.tofs[t];
-    c = row_count(tr, cur.tnnz[t], k);
+    c = tail_count(tr, cur.tnnz[t], k);
   }
   return ((double)c + d.beta) / d.den[k];
 }
@@ -595,7 +603,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 #pragma unroll 4
   for (uint32_t e = 0; e < nnz; ++e) {
     const uint32_t w = __ldg(E + e);
-    const uint32_t k = w >> 16;
+    const uint32_t k = d_topic(w);
     if (k != K1) Sp = Sp + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
   }
   const double Z = (M + Sp) + rec.Qp;
@@ -611,7 +619,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
     uint32_t last = K1;
     for (uint32_t e = 0; e < nnz; ++e) {
       const uint32_t w = __ldg(E + e);
-      const uint32_t k = w >> 16;
+      const uint32_t k = d_topic(w);
       if (k == K1) continue;
       acc = acc + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
       last = k;
@@ -806,7 +814,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             const uint32_t w = wv[e];
             if (topic == 0xFFFFFFFFu && w != 0u) {
               const unsigned long long q = entry_mac(w, row_s, pa);
-              if ((w >> 16) != K1 && q > Yf) topic = w >> 16;
+              if (d_topic(w) != K1 && q > Yf) topic = d_topic(w);
               else pb = q;
               pa = q;
             }
@@ -818,8 +826,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             const uint32_t w = __ldg(E + e);
             const unsigned long long q = entry_mac(w, row_s, pa);
             pa = q;
-            if ((w >> 16) != K1 && q > Yf) {
-              topic = w >> 16;
+            if (d_topic(w) != K1 && q > Yf) {
+              topic = d_topic(w);
               break;
             }
             pb = q;
@@ -1164,7 +1172,7 @@ __device__ void item_epilogue(const Dev& d, const Buf& nxt, uint32_t v, const ui
     }
   } else {
     const uint32_t t = v - d.Vd;
-    const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, s_run);
+    const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, s_run, 16u);
     if (tid == 0) nxt.tnnz[t] = nz;
     for (uint32_t k = tid; k < d.K; k += blockDim.x) {
       const uint32_t c = hist[k];
@@ -1217,7 +1225,7 @@ __global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double
     for (uint32_t c = 0; c * 32u < nnz; ++c) {
       const uint32_t i = c * 32u + lane;
       const uint32_t e = (i < nnz) ? Drow[i] : 0u;
-      const double w = (i < nnz) ? (double)(e & 0xFFFFu) * row[e >> 16] : 0.0;
+      const double w = (i < nnz) ? (double)(e & 0xFFFFu) * row[d_topic(e)] : 0.0;
       carry = carry + __shfl_sync(kFull, warp_incl_scan(w), 31);
     }
     const double p = (carry + Qfull) / ((double)L + Kalpha);

@@ -10,7 +10,7 @@
 //     capacity 8 + roundup8(min(L_d, K)) words; entries start 32-byte aligned after an
 //     8-word header and are zero padded to a multiple of 8 entries, so the sampler reads
 //     whole sectors without masking):
-//     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+8+i] = (topic << 16) | count
+//     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+8+i] = (topic << 18) | count
 //     sorted by topic (packed CSR; rebuilt every iteration)
 //   word-major runs r in [0, R) (runs of word v contiguous, ordered by doc length desc):
 //     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
@@ -31,6 +31,11 @@
 namespace ezl {
 
 constexpr uint16_t kUnsampled = 0xFFFFu;  // z^i of a token the sampler must draw (K <= 65535)
+// packed D entry: (topic << kDT) | count, count < 2^16, topic < 2^14 (K <= 16384): the
+// byte offset of topic in a u32 table is then simply entry >> 16 (one LEA.HI per gather)
+constexpr uint32_t kDT = 18;
+__host__ __device__ __forceinline__ uint32_t d_entry(uint32_t k, uint32_t c) { return (k << kDT) | c; }
+__host__ __device__ __forceinline__ uint32_t d_topic(uint32_t w) { return w >> kDT; }
 constexpr uint32_t kDHdr = 8;  // header words in front of every packed D row (one 32 B sector)
 #ifndef EZLDA_SEGCAP
 #define EZLDA_SEGCAP 256
