@@ -645,9 +645,15 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
-  // What' | QP rows for every word when they fit in 8 GiB (the sampler then stages every
-  // item with one bulk copy), else for the dense words only (tail rows staged by a warp)
-  d.Vw = ((uint64_t)h->V * d.rs * 8ull <= (8ull << 30)) ? h->V : h->Vd;
+  // fixed-point What' | QP rows for every word when they fit in a quarter of the free device
+  // memory, at most 32 GiB (the sampler then stages every item with one bulk copy), else for
+  // the dense words only (tail rows staged by a warp)
+  {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
+    const uint64_t budget = std::min<uint64_t>(32ull << 30, fr / 4);
+    d.Vw = ((uint64_t)h->V * d.rs * 8ull <= budget) ? h->V : h->Vd;
+  }
   EZ_ALLOC(h, d.wrow, double, (size_t)d.Vw * d.rs);
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
