@@ -259,6 +259,27 @@ __device__ __forceinline__ uint32_t row_lookup(const uint16_t* keys, const uint1
   return (lo < n && keys[lo] == k) ? cnts[lo] : 0u;
 }
 
+// MPT test of one token j (word v, run rid) of a doc of length L.  C(k) = D[d][k].
+template <typename LookupF>
+__device__ __forceinline__ void mpt_token(const Dev& d, const Buf& nxt, uint32_t j, uint32_t L, uint32_t iter,
+                                          uint32_t v, uint32_t rid, LookupF C, unsigned long long& n_skip) {
+  const WordRec r = d.rec[v];
+  const uint32_t C1 = C(r.K[0]);
+  const uint32_t C2 = d.geff >= 2 ? C(r.K[1]) : 0u;
+  const uint32_t C3 = d.geff >= 3 ? C(r.K[2]) : 0u;
+  const double M = mpt_M(r, C1, d.alpha);
+  const double den = mpt_den(r, M, C1, C2, C3, L, d.geff);
+  const double u = philox_u(d.seed, iter, d.token_base + j);
+  if (mpt_skip(u, M, den)) {
+    nxt.z[j] = r.K[0];
+    ++n_skip;
+  } else {
+    // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
+    nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, 0x7FFFu)) : kUnsampled;
+    atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
+  }
+}
+
 // Per-token MPT test of one doc's tokens (shared by both doc tiers).  C(k) = D[d][k].
 template <typename LookupF>
 __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nxt, uint32_t j0, uint32_t L,
@@ -292,7 +313,10 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
 // 32-topic words: popcount prefix + set-bit walk, O(nnz + K/32) per doc) and both are
 // re-zeroed as they are read.
 template <bool kSkipTest>
-__global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
+#ifndef EZLDA_DOC_MINB
+#define EZLDA_DOC_MINB 1
+#endif
+__global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
                                                               uint32_t n_docs, uint32_t iter) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -307,15 +331,38 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_hist(Dev d, Buf cur, Buf
     const uint32_t doc = docs[idx];
     const uint32_t j0 = d.dofs[doc];
     const uint32_t L = d.dofs[doc + 1] - j0;
-    for (uint32_t i = lane; i < L; i += 32) {
+    // the first kPre tokens of each lane: topic, word and run id loaded together (the
+    // skip test's word records then depend on one load round instead of two)
+    constexpr uint32_t kPre = 4;
+    uint32_t pk[kPre], pv[kPre], pr[kPre];
+#pragma unroll
+    for (uint32_t c = 0; c < kPre; ++c) {
+      const uint32_t i = lane + 32u * c;
+      pk[c] = (i < L) ? cur.z[j0 + i] : 0u;
+      pv[c] = (kSkipTest && i < L) ? d.tw[j0 + i] : 0u;
+      pr[c] = (kSkipTest && i < L) ? d.trid[j0 + i] : 0u;
+    }
+#pragma unroll
+    for (uint32_t c = 0; c < kPre; ++c) {
+      if (lane + 32u * c < L) {
+        const uint32_t k = pk[c];
+        atomicAdd(&hist[k >> 1], 1u << ((k & 1u) << 4));
+        atomicOr(&bmp[k >> 5], 1u << (k & 31u));
+      }
+    }
+    for (uint32_t i = lane + 32u * kPre; i < L; i += 32) {
       const uint32_t k = cur.z[j0 + i];
       atomicAdd(&hist[k >> 1], 1u << ((k & 1u) << 4));
       atomicOr(&bmp[k >> 5], 1u << (k & 31u));
     }
     __syncwarp();
     if (kSkipTest) {
-      doc_tokens_skip_test(d, nxt, j0, L, iter, lane, 32,
-                           [&](uint32_t k) { return (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu; }, n_skip);
+      auto C = [&](uint32_t k) { return (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu; };
+#pragma unroll
+      for (uint32_t c = 0; c < kPre; ++c)
+        if (lane + 32u * c < L) mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], pr[c], C, n_skip);
+      for (uint32_t i = lane + 32u * kPre; i < L; i += 32)
+        mpt_token(d, nxt, j0 + i, L, iter, d.tw[j0 + i], d.trid[j0 + i], C, n_skip);
       __syncwarp();
     }
     uint32_t* Drow = d.D + d.ddb[doc] + kDHdr;
