@@ -774,10 +774,11 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
+    // only as many steps as the longest run piece in this round needs (runs are short)
+    const uint32_t span = __reduce_max_sync(kFull, lane - rs + 1u);
+    for (uint32_t o = 1; o < span; o <<= 1) {
       const unsigned long long y = __shfl_up_sync(kFull, acc, o);
-      if (lane >= rs + (uint32_t)o) acc += y;
+      if (lane >= rs + o) acc += y;
     }
     const bool cont = s_soff < B0;  // the run started in an earlier round
     if (cont) acc += carry;
