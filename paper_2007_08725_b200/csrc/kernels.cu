@@ -153,14 +153,15 @@ __global__ void k_den(Dev d, Buf cur) {
   }
 }
 
-// H1: word-prep ("MPT generate", P:546 step 1).  One warp per word: stage the What row
+// H1: word-prep, small K (K <= 4096).  One warp per word: stage the What row
 // in shared memory, top-4 (value desc, topic asc) by per-lane insertion + a 4-round warp
 // tournament, What' (K1 entry zeroed), then lane 0 runs the Q' prefix P_v(k) strictly
 // sequentially (the oracle's order: QP[k] = alpha P_v(k), Q' = alpha P_v(K-1) bit for bit)
 // while the other warps of the SM proceed with their words.
 constexpr uint32_t kWpWarps = 4;
+constexpr uint32_t kWpSmallK = 4096;  // warp-per-word word-prep up to this K, thread-per-word above
 
-__global__ void __launch_bounds__(kWpWarps * 32) k_word_prep(Dev d, Buf cur) {
+__global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t v = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -244,6 +245,87 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep(Dev d, Buf cur) {
     }
     d.rec[v] = r;
   }
+}
+
+// H1: word-prep, large K.  One THREAD per word: the word's What
+// values are formed on the fly in ascending topic order (dense rows: (W + beta) / den_k;
+// tail rows: the absent-pair value beta / den_k merged with the sorted nonzeros), pass 1
+// keeps the top-4 (value desc, topic asc), pass 2 writes the fixed-point What' row for the
+// sampler and runs the Q' prefix P_v(k) strictly sequentially -- the oracle's order, so
+// QP[k] = alpha P_v(k) and Q' = alpha P_v(K-1) are its values bit for bit.  32 words per
+// warp run their sequential chains side by side (all lanes busy).
+struct WhatCursor {  // What[v][k] for ascending k
+  const int32_t* wd;    // dense row or nullptr
+  const uint32_t* tr;   // tail packed row (topic << 16 | count)
+  uint32_t n, e, nk;    // tail nnz, cursor, next nonzero topic (0xFFFFFFFF: none)
+};
+
+__device__ __forceinline__ double what_next(const Dev& d, WhatCursor& c, uint32_t k) {
+  if (c.wd) return ((double)c.wd[k] + d.beta) / d.den[k];
+  if (k == c.nk) {
+    const uint32_t p = c.tr[c.e];
+    ++c.e;
+    c.nk = (c.e < c.n) ? (c.tr[c.e] >> 16) : 0xFFFFFFFFu;
+    return ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
+  }
+  return __ldg(d.what0 + k);
+}
+
+__device__ __forceinline__ void what_reset(const Dev& d, const Buf& cur, uint32_t v, WhatCursor& c) {
+  if (v < d.Vd) {
+    c.wd = cur.Wd + (size_t)v * d.K;
+    c.tr = nullptr;
+    c.n = c.e = 0;
+    c.nk = 0xFFFFFFFFu;
+  } else {
+    const uint32_t t = v - d.Vd;
+    c.wd = nullptr;
+    c.tr = cur.Wt + d.tofs[t];
+    c.n = cur.tnnz[t];
+    c.e = 0;
+    c.nk = c.n ? (c.tr[0] >> 16) : 0xFFFFFFFFu;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= d.V || d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard
+  WhatCursor c;
+  what_reset(d, cur, v, c);
+  Top4 t;
+  top4_init(t);
+  for (uint32_t k = 0; k < d.K; ++k) top4_insert(t, what_next(d, c, k), k);
+  WordRec r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool ok = t.v[i] >= 0.0;
+    r.a[i] = ok ? t.v[i] : 0.0;
+    r.K[i] = ok ? (uint16_t)t.k[i] : (uint16_t)0;
+  }
+  const uint32_t K1 = r.K[0];
+  const bool out = v < d.Vw;
+  uint32_t* outm = reinterpret_cast<uint32_t*>(d.wrow + (size_t)v * d.rs);
+  double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
+  int e = 0;
+  frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
+  const int sh = 32 - e;
+  if (out) {
+    outq[d.Kpad] = ldexp(1.0, -sh);
+    outq[d.Kpad + 1u] = ldexp(1.0, sh);
+  }
+  what_reset(d, cur, v, c);
+  double acc = 0.0;
+  for (uint32_t k = 0; k < d.Kpad; ++k) {
+    double w = (k < d.K) ? what_next(d, c, k) : 0.0;
+    if (k == K1) w = 0.0;  // What' (Eq 6): the maximum entry set to 0
+    acc = acc + w;
+    if (k == d.K - 1u) r.Qp = d.alpha * acc;
+    if (out) {
+      outm[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
+      outq[k] = d.alpha * acc;
+    }
+  }
+  d.rec[v] = r;
 }
 
 // ---------------------------------------------------------------------------------
@@ -1321,11 +1403,6 @@ __global__ void k_topics_from_input(const uint16_t* in, const uint32_t* perm, ui
 
 }  // namespace
 
-static uint32_t word_prep_warps(uint32_t K) {  // words (warps) per block: their rows must fit in smem
-  const size_t row = (size_t)((K + 31) / 32) * 32 * 8;
-  return (uint32_t)std::max<size_t>(1, std::min<size_t>(kWpWarps, (227u * 1024u) / row));
-}
-size_t word_prep_smem_bytes(uint32_t K) { return (size_t)word_prep_warps(K) * ((K + 31) / 32) * 32 * 8; }
 size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
@@ -1352,10 +1429,14 @@ size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 
 static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
 static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
 
+size_t word_prep_smem_bytes(uint32_t K) { return (size_t)kWpWarps * ((K + 31) / 32) * 32 * 8; }  // row per warp
+
 cudaError_t configure_kernels(uint32_t K) {
   cudaError_t e;
-  const int wp = (int)word_prep_smem_bytes(K), sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
-  if ((e = cudaFuncSetAttribute(k_word_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, wp))) return e;
+  if (K <= kWpSmallK &&
+      (e = cudaFuncSetAttribute(k_word_prep_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)word_prep_smem_bytes(K))))
+    return e;
+  const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)llpt_smem_bytes(K)))) return e;
   if ((e = cudaFuncSetAttribute(k_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
   {
@@ -1383,8 +1464,11 @@ void launch_den(const Dev& d, const Buf& cur, cudaStream_t s) {
 }
 
 void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s) {
-  const uint32_t wpw = word_prep_warps(d.K);
-  k_word_prep<<<(d.V + wpw - 1) / wpw, wpw * 32, word_prep_smem_bytes(d.K), s>>>(d, cur);
+  if (d.K <= kWpSmallK) {
+    k_word_prep_w<<<(d.V + kWpWarps - 1) / kWpWarps, kWpWarps * 32, word_prep_smem_bytes(d.K), s>>>(d, cur);
+  } else {
+    k_word_prep_t<<<(d.V + 127) / 128, 128, 0, s>>>(d, cur);
+  }
 }
 
 void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_t* docs_w, uint32_t n_w,

@@ -112,7 +112,6 @@ size_t sampler_smem_bytes(uint32_t K);
 uint32_t sampler_slots(uint32_t K);  // pipelined item slots per sampler block (0: K too large)
 uint32_t wrow_stride(uint32_t K);
 uint32_t seg_width(uint32_t K);
-size_t word_prep_smem_bytes(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);
 cudaError_t configure_kernels(uint32_t K);
 
