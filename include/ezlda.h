@@ -32,9 +32,8 @@
  *     and the stream given in the options (or one it creates).
  *   - Threading: one handle per host thread; calls on a handle are serialised.
  *   - Limits (16+16-bit packing): K <= 65535, doc length <= 65535,
- *     tokens per shard < 2^32.  This build additionally requires K <= 11200
- *     (the staged fp32 What' row and fp64 Q' table of a sampler item must fit in
- *     shared memory; NEXT-2 lifts it).
+ *     tokens per shard < 2^32.  This build additionally requires K <= 16384 (the
+ *     packed D entries hold the topic in 14 bits; NEXT-2 lifts it).
  */
 #ifndef EZLDA_H
 #define EZLDA_H

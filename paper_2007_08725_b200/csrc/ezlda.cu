@@ -327,7 +327,13 @@ void fill_dev(ezlda* h) {
   d.rs = ezl::wrow_stride(h->K);
   d.segw = ezl::seg_width(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
-  d.nslots = ezl::sampler_slots(h->K);
+  {
+    const ezl::SamplerLayout L = ezl::sampler_layout(h->K);
+    d.nslots = L.nslots;
+    d.hist_global = L.hist_global;
+    d.slot_bytes = L.slot_bytes;
+    d.ws_bytes = L.ws_bytes;
+  }
   d.exact_all = h->exact_all;
   d.geff = std::min<uint32_t>(h->g, h->K - 1);
   d.alpha = h->alpha;
@@ -679,6 +685,13 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(d_cnt);
   h->release(d_max);
   EZ_CUDA(h, ezl::configure_kernels(h->K));
+  {  // per-(sampler block, slot) scratch: HBM histograms (large K) and exact Q' tables of
+     // warp-staged tail rows
+    const size_t n = (size_t)ezl::sampler_grid_size() * d.nslots * d.Kpad;
+    EZ_ALLOC(h, d.hist_scratch, uint32_t, n);
+    EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, n * sizeof(uint32_t), s));
+    EZ_ALLOC(h, d.qp_scratch, double, n);
+  }
   // ---- iteration 0
   h->cur = 0;
   ezl::launch_init_topics(d, h->buf[0].z, s);
@@ -783,8 +796,8 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   if (n_tokens == 0 || K == 0 || V == 0 || n_docs == 0) return bad(EZLDA_E_INVALID, "n_tokens, K, V and n_docs must be > 0");
   if (!(alpha > 0.0) || !(beta > 0.0)) return bad(EZLDA_E_INVALID, "alpha and beta must be > 0");
   if (K > 65535) return bad(EZLDA_E_RANGE, "K > 65535 (16-bit topic packing, P:753)");
-  if (ezl::sampler_slots(K) == 0)
-    return bad(EZLDA_E_RANGE, "K > 11200 not supported by this build (staged What' row + Q' table, NEXT-2)");
+  if (K > 16384 || ezl::sampler_slots(K) == 0)
+    return bad(EZLDA_E_RANGE, "K > 16384 not supported by this build (14-bit topic field of the packed D entries)");
   if (n_tokens >= (1ull << 32)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^32 per shard");
   ezlda_options o{};
   if (opts) {  // struct_size versioning: a smaller (older) struct leaves the new fields zero

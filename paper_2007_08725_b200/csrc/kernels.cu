@@ -153,6 +153,25 @@ __global__ void k_den(Dev d, Buf cur) {
   }
 }
 
+// wrow record of word v (u32 m | u32 qfx | f64 scales {2^-s, 2^s, 2^-t, 2^t} | f64 QP):
+// the first three parts are one bulk copy into a sampler slot; QP (exact) stays in HBM for
+// the exact redraws.
+struct WrowPtrs {
+  uint32_t* m;
+  uint32_t* qfx;
+  double* sc;
+  double* qp;
+};
+__device__ __forceinline__ WrowPtrs wrow_ptrs(const Dev& d, uint32_t v) {
+  double* b = d.wrow + (size_t)v * d.rs;
+  WrowPtrs o;
+  o.m = reinterpret_cast<uint32_t*>(b);
+  o.qfx = o.m + d.Kpad;
+  o.sc = b + d.Kpad;
+  o.qp = o.sc + 4;
+  return o;
+}
+
 // H1: word-prep, small K (K <= 4096).  One warp per word: stage the What row
 // in shared memory, top-4 (value desc, topic asc) by per-lane insertion + a 4-round warp
 // tournament, What' (K1 entry zeroed), then lane 0 runs the Q' prefix P_v(k) strictly
@@ -211,19 +230,19 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
   if (lane == 0) row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
   __syncwarp();
   const bool out = v < d.Vw;
-  uint32_t* outm = reinterpret_cast<uint32_t*>(d.wrow + (size_t)v * d.rs);
-  double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
+  WrowPtrs o = wrow_ptrs(d, v);
   if (out) {  // fixed-point What'[v] (m = rint(What' 2^s), s from max What' = a2) + scale
     int e = 0;
     frexp(r.a[1], &e);
     const int sh = 32 - e;  // max What' 2^sh in [2^31, 2^32)
     for (uint32_t k = lane; k < d.Kpad; k += 32u)
-      outm[k] = __double2uint_rn(fmin(ldexp(row[k], sh), 4294967295.0));
+      o.m[k] = __double2uint_rn(fmin(ldexp(row[k], sh), 4294967295.0));
     if (lane == 0) {
-      outq[d.Kpad] = ldexp(1.0, -sh);
-      outq[d.Kpad + 1u] = ldexp(1.0, sh);
+      o.sc[0] = ldexp(1.0, -sh);
+      o.sc[1] = ldexp(1.0, sh);
     }
   }
+  double* outq = o.qp;
   if (lane == 0) {
     // Q' prefix, strictly sequential; the next 8 entries are loaded before the dependent adds
     double acc = 0.0, x[8];
@@ -244,6 +263,17 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
       for (int i = 0; i < 8; ++i) x[i] = xn[i];
     }
     d.rec[v] = r;
+    if (out) {
+      int e = 0;
+      frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
+      o.sc[2] = ldexp(1.0, e - 32);
+      o.sc[3] = ldexp(1.0, 32 - e);
+    }
+  }
+  if (out) {
+    __syncwarp();
+    const double two_t = o.sc[3];
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(outq[k] * two_t, 4294967295.0));
   }
 }
 
@@ -304,14 +334,13 @@ __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
   }
   const uint32_t K1 = r.K[0];
   const bool out = v < d.Vw;
-  uint32_t* outm = reinterpret_cast<uint32_t*>(d.wrow + (size_t)v * d.rs);
-  double* outq = d.wrow + (size_t)v * d.rs + d.Kpad / 2u;
+  WrowPtrs o = wrow_ptrs(d, v);
   int e = 0;
   frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
   const int sh = 32 - e;
   if (out) {
-    outq[d.Kpad] = ldexp(1.0, -sh);
-    outq[d.Kpad + 1u] = ldexp(1.0, sh);
+    o.sc[0] = ldexp(1.0, -sh);
+    o.sc[1] = ldexp(1.0, sh);
   }
   what_reset(d, cur, v, c);
   double acc = 0.0;
@@ -321,11 +350,18 @@ __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
     acc = acc + w;
     if (k == d.K - 1u) r.Qp = d.alpha * acc;
     if (out) {
-      outm[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
-      outq[k] = d.alpha * acc;
+      o.m[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
+      o.qp[k] = d.alpha * acc;
     }
   }
   d.rec[v] = r;
+  if (out) {
+    frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
+    const double two_t = ldexp(1.0, 32 - e);
+    o.sc[2] = ldexp(1.0, e - 32);
+    o.sc[3] = two_t;
+    for (uint32_t k = 0; k < d.Kpad; ++k) o.qfx[k] = __double2uint_rn(fmin(o.qp[k] * two_t, 4294967295.0));
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -629,9 +665,9 @@ struct RunCounters {
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct __align__(16) WarpScratch {
-  unsigned long long P[2 * kSegCap];  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
-  uint32_t q[kQueue];     // queue of flagged runs
+struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | queue
+  unsigned long long* P;  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
+  uint32_t* q;            // queue of flagged runs
 };
 
 // 32-byte (one sector) read-only load
@@ -778,9 +814,9 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 // is redrawn by exact_draw.  Either way the topic equals the oracle's fp64 decision.
 template <uint32_t kSegW>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
-                                                 uint32_t v, uint32_t row_s, const double* QP, double inv_s,
-                                                 double two_s, uint32_t* hist, WarpScratch& ws, uint32_t qn,
-                                                 uint32_t iter, RunCounters& rc) {
+                                                 uint32_t v, uint32_t row_s, const uint32_t* qfx, const double* scl,
+                                                 const double* const* qpp, uint32_t* hist, WarpScratch& ws,
+                                                 uint32_t qn, uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
   // ---- A: lane per run: run table + header, segment admission
@@ -856,11 +892,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
-    // only as many steps as the longest run piece in this round needs (runs are short)
-    const uint32_t span = __reduce_max_sync(kFull, lane - rs + 1u);
-    for (uint32_t o = 1; o < span; o <<= 1) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long y = __shfl_up_sync(kFull, acc, o);
-      if (lane >= rs + o) acc += y;
+      if (lane >= rs + (uint32_t)o) acc += y;
     }
     const bool cont = s_soff < B0;  // the run started in an earlier round
     if (cont) acc += carry;
@@ -882,6 +917,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   //      32768 (d.zmark), else 0xFFFF.
   const double Qp = rec.Qp;
   for (uint32_t B0 = 0; B0 < ntb; B0 += 32u) {
+    const double inv_s = scl[0];  // fixed-point scale of m (shared memory, broadcast)
     const uint32_t slot = slot_of(B0, tofs);
     const uint32_t s_j0 = __shfl_sync(kFull, j0, slot);
     const uint32_t s_tofs = __shfl_sync(kFull, tofs, slot);
@@ -927,7 +963,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         // S' branch: first checkpoint with P > y, then the walk from the previous one, all
         // in exact integers against Yf = floor(y 2^s)  (P > y  <=>  P > Yf for integer P)
         const double y = x - M;
-        const unsigned long long Yf = (unsigned long long)(y * two_s);
+        const unsigned long long Yf = (unsigned long long)(y * scl[1]);
         uint32_t a = c0, b = c0 + nck - 1u;
         while (a < b) {
           const uint32_t mid = (a + b) >> 1;
@@ -967,20 +1003,26 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         if (topic != 0xFFFFFFFFu && !((double)pa * inv_s - y > mg && y - (double)pb * inv_s > mg))
           topic = 0xFFFFFFFFu;  // uncertified: exact redraw
       } else {
-        // Q' branch: first topic k != K1 with alpha P(k) > y (binary search over QP, which
-        // is flat across K1 and holds the oracle's values)
+        // Q' branch: first topic k != K1 with alpha P(k) > y, searched over the fixed-point
+        // copy qfx = rint(QP 2^t) of the oracle's prefix table (flat across K1) against
+        // Yq = floor(y 2^t); certified with the margin widened by qfx's one-ulp error
         const double y = (x - M) - Sp;
-        uint32_t a = 0, b = d.Kpad - 1u;
-        while (a < b) {
-          const uint32_t mid = (a + b) >> 1;
-          if (QP[mid] > y) b = mid; else a = mid + 1u;
+        if (y >= 0.0) {
+          const double inv_t = scl[2];
+          const uint32_t Yq = (uint32_t)fmin(y * scl[3], 4294967295.0);  // past the end: uncertified
+          uint32_t a = 0, b = d.Kpad - 1u;
+          while (a < b) {
+            const uint32_t mid = (a + b) >> 1;
+            if (qfx[mid] > Yq) b = mid; else a = mid + 1u;
+          }
+          const double mq = mg + inv_t;
+          const double qa = (double)qfx[a] * inv_t, qp = a ? (double)qfx[a - 1u] * inv_t : 0.0;
+          if (a != K1 && a < d.K && qa - y > mq && y - qp > mq) topic = a;
         }
-        const double prev = a ? QP[a - 1u] : 0.0;
-        if (a != K1 && a < d.K && QP[a] - y > mg && y - prev > mg) topic = a;
       }
     }
     if (topic == 0xFFFFFFFFu) {
-      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, QP, hit);
+      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, *qpp, hit);
       rc.exact += 1;
     }
     if (hit) rc.hitM += 1;
@@ -1015,6 +1057,7 @@ struct __align__(16) SlotCtl {
   uint32_t cursor, done;
   uint32_t sampled, hitM, runs, words, exact;
   uint32_t state;  // block item number held by the slot (| kExit: no item left)
+  const double* qp;  // exact Q' prefix table of the item's word (HBM)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t* p) {
@@ -1029,15 +1072,15 @@ __device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
                : "memory");
 }
 
-// per-slot dynamic shared memory: m u32 [Kpad] | QP f64 [Kpad] | (2^-s, 2^s) f64 | hist u32 [Kpad]
-// (m | QP | scale is one bulk copy of a wrow record)
-__host__ __device__ __forceinline__ uint32_t slot_bytes(uint32_t K) { return 16u * ((K + 31u) / 32u) * 32u + 16u; }
+// per-slot dynamic shared memory: m u32 [Kpad] | qfx u32 [Kpad] | scales f64 [4] (one bulk
+// copy of the word's wrow record head) | hist u32 [Kpad] when it fits (else in HBM scratch)
+__host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad) { return 8u * Kpad + 32u; }
 
 // Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
-// fixed-point What' row + scale and the sequential Q' prefix QP, the same expressions and
-// order as k_word_prep (QP doubles as the fp64 row while lane 0 runs the prefix in place).
+// fixed-point What' row, the sequential Q' prefix (the same expressions and order as
+// k_word_prep) into the slot's HBM scratch QP, its fixed-point copy and the scales.
 __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, uint32_t* m,
-                                    double* QP) {
+                                    uint32_t* qfx, double* sc, double* QP) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
   for (uint32_t k0 = lane; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane
@@ -1067,10 +1110,6 @@ __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, co
   frexp(rec.a[1], &e);
   const int sh = 32 - e;
   for (uint32_t k = lane; k < d.Kpad; k += 32u) m[k] = __double2uint_rn(fmin(ldexp(QP[k], sh), 4294967295.0));
-  if (lane == 0) {
-    QP[d.Kpad] = ldexp(1.0, -sh);
-    QP[d.Kpad + 1u] = ldexp(1.0, sh);
-  }
   __syncwarp();
   if (lane == 0) {
     double acc = 0.0;
@@ -1082,12 +1121,24 @@ __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, co
   }
   __syncwarp();
   for (uint32_t k = lane; k < d.Kpad; k += 32u) QP[k] = d.alpha * QP[k];
+  int et = 0;
+  frexp(rec.Qp, &et);
+  const double two_t = ldexp(1.0, 32 - et);
+  __syncwarp();
+  for (uint32_t k = lane; k < d.Kpad; k += 32u) qfx[k] = __double2uint_rn(fmin(QP[k] * two_t, 4294967295.0));
+  if (lane == 0) {
+    sc[0] = ldexp(1.0, -sh);
+    sc[1] = ldexp(1.0, sh);
+    sc[2] = ldexp(1.0, et - 32);
+    sc[3] = two_t;
+  }
   __syncwarp();
 }
 
 // Arm slot `sl` with block item k (one warp): claim the next global item, publish its
 // description, start the What' row transfer.  The slot's histogram is zero on entry.
-__device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char* sbase, uint32_t k, uint32_t n_items) {
+__device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char* sbase, double* qp_scratch, uint32_t k,
+                         uint32_t n_items) {
   const uint32_t lane = threadIdx.x & 31u;
   uint32_t i = 0;
   if (lane == 0) i = (uint32_t)atomicAdd(&d.ctr->item_ctr, 1ull);
@@ -1098,7 +1149,6 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
   }
   const uint32_t v = d.item_word[i];
   uint32_t* mrow = reinterpret_cast<uint32_t*>(sbase);
-  double* QP = reinterpret_cast<double*>(sbase + 4u * d.Kpad);
   const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&c.mbar);
   if (lane < 6) reinterpret_cast<uint64_t*>(&c.rec)[lane] = reinterpret_cast<const uint64_t*>(d.rec + v)[lane];
   if (lane == 0) {
@@ -1115,10 +1165,15 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
     c.exact = 0;
   }
   if (v < d.Vw) {  // precomputed by word-prep
-    if (lane == 0) bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, d.rs * 8u, mbar_s);
+    if (lane == 0) {
+      c.qp = wrow_ptrs(d, v).qp;
+      bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, slot_head_bytes(d.Kpad), mbar_s);
+    }
   } else {
+    if (lane == 0) c.qp = qp_scratch;
     __syncwarp();
-    stage_tail_row_warp(d, cur, v, c.rec, mrow, QP);
+    stage_tail_row_warp(d, cur, v, c.rec, mrow, mrow + d.Kpad, reinterpret_cast<double*>(mrow + 2u * d.Kpad),
+                        qp_scratch);
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
   }
   __syncwarp();
@@ -1175,8 +1230,8 @@ __device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uin
 #endif
 constexpr int kSampWarpsP = EZLDA_SAMP_WARPS;
 
-__host__ __device__ __forceinline__ uint32_t sampler_ws_offset(uint32_t K, uint32_t nslots) {
-  return (uint32_t)((sizeof(SlotCtl) * kMaxSlots + 15u) & ~15u) + nslots * slot_bytes(K);
+__host__ __device__ __forceinline__ uint32_t sampler_ctl_bytes() {
+  return (uint32_t)((sizeof(SlotCtl) * kMaxSlots + 15u) & ~15u);
 }
 
 #ifndef EZLDA_SAMP_MINB
@@ -1187,11 +1242,22 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
                                                                   uint32_t n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
   SlotCtl* ctl = reinterpret_cast<SlotCtl*>(smem);
-  unsigned char* slots = smem + ((sizeof(SlotCtl) * kMaxSlots + 15u) & ~15u);
-  const uint32_t sb = slot_bytes(d.K);
+  unsigned char* slots = smem + sampler_ctl_bytes();
+  const uint32_t sb = d.slot_bytes;
   const uint32_t nsl = d.nslots;
-  WarpScratch* s_ws = reinterpret_cast<WarpScratch*>(smem + sampler_ws_offset(d.K, nsl));
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  WarpScratch ws;
+  {
+    unsigned char* wb = slots + nsl * sb + warp * d.ws_bytes;
+    ws.P = reinterpret_cast<unsigned long long*>(wb);
+    ws.q = reinterpret_cast<uint32_t*>(wb + d.ws_bytes - 4u * kQueue);
+  }
+  // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
+  auto hist_of = [&](uint32_t sl) -> uint32_t* {
+    return d.hist_global ? d.hist_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad
+                         : reinterpret_cast<uint32_t*>(slots + sl * sb + slot_head_bytes(d.Kpad));
+  };
+  auto qps_of = [&](uint32_t sl) -> double* { return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad; };
   const uint32_t nw = blockDim.x >> 5;
   // prologue: barriers, zero histograms, warp 0 arms the first kSlots items
   if (tid == 0) {
@@ -1202,14 +1268,14 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (uint32_t sl = 0; sl < nsl; ++sl) {
-    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad + 16u);
-    for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
-  }
+  if (!d.hist_global)  // (the HBM scratch histograms are zeroed at create and by every epilogue)
+    for (uint32_t sl = 0; sl < nsl; ++sl) {
+      uint32_t* hist = hist_of(sl);
+      for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+    }
   __syncthreads();
   if (warp == 0)
-    for (uint32_t sl = 0; sl < nsl; ++sl) arm_slot(d, cur, ctl[sl], slots + sl * sb, sl, n_items);
-  WarpScratch& ws = s_ws[warp];
+    for (uint32_t sl = 0; sl < nsl; ++sl) arm_slot(d, cur, ctl[sl], slots + sl * sb, qps_of(sl), sl, n_items);
   for (uint32_t k = 0;; ++k) {
     const uint32_t sl = k % nsl;
     SlotCtl& c = ctl[sl];
@@ -1220,9 +1286,9 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     st = __shfl_sync(kFull, st, 0);
     if (st & kExit) break;
     mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
-    const double* QP = reinterpret_cast<const double*>(slots + sl * sb + 4u * d.Kpad);
-    const double inv_s = QP[d.Kpad], two_s = QP[d.Kpad + 1u];  // fixed-point scale of m
-    uint32_t* hist = reinterpret_cast<uint32_t*>(slots + sl * sb + 12u * d.Kpad + 16u);
+    const uint32_t* qfx = reinterpret_cast<const uint32_t*>(slots + sl * sb + 4u * d.Kpad);
+    const double* scl = reinterpret_cast<const double*>(slots + sl * sb + 8u * d.Kpad);
+    uint32_t* hist = hist_of(sl);
     const WordRec rec = c.rec;
     const uint32_t v = c.v, r0 = c.r0, r1 = c.r1;
     const uint32_t row_s = (uint32_t)__cvta_generic_to_shared(slots + sl * sb);
@@ -1250,11 +1316,11 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
       if (qn == 0) break;
       uint32_t nb;
       switch (d.segw) {
-        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
-        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
-        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
-        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
-        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, QP, inv_s, two_s, hist, ws, qn, iter, rc); break;
+        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
+        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
+        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
+        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
+        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
       }
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
@@ -1281,7 +1347,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     last = __shfl_sync(kFull, last, 0);
     if (last) {
       item_epilogue_warp(d, nxt, c, hist);
-      arm_slot(d, cur, c, slots + sl * sb, k + nsl, n_items);
+      arm_slot(d, cur, c, slots + sl * sb, qps_of(sl), k + nsl, n_items);
     }
   }
 }
@@ -1407,27 +1473,41 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-uint32_t wrow_stride(uint32_t K) { return 3u * ((K + 31) / 32) * 16 + 2u; }  // m u32 | QP | scale (doubles)
+uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32 + 4u; }  // m | qfx | scales | QP (doubles)
 uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= 16 with K <= kSegCap segw
   uint32_t w = 16u;
   while (w * kSegCap < K) w <<= 1;
   return w;
 }
-static size_t sampler_smem_bytes_n(uint32_t K, uint32_t nslots) {
-  return sampler_ws_offset(K, nslots) + sizeof(WarpScratch) * kSampWarpsP;
-}
 constexpr size_t kMaxSmem = 227u * 1024u;
-uint32_t sampler_slots(uint32_t K) {  // 0: does not fit
-  for (uint32_t n = kMaxSlots; n >= 1; --n)
-    if (sampler_smem_bytes_n(K, n) <= kMaxSmem) return n;
-  return 0;
+// shared-memory layout of the sampler block: kMaxSlots SlotCtl | nslots x (slot head [+ hist])
+// | kSampWarpsP x warp scratch.  Two slots with the histograms in shared memory when they fit,
+// else two slots with the histograms in HBM scratch, else one slot.
+SamplerLayout sampler_layout(uint32_t K) {
+  SamplerLayout L{};
+  const uint32_t Kpad = (K + 31) / 32 * 32;
+  L.ws_bytes = (seg_width(K) == 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
+  const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
+  const uint32_t head = slot_head_bytes(Kpad), with_hist = head + 4u * Kpad;
+  for (uint32_t n = kMaxSlots; n >= 1; --n) {
+    if (fixed + (size_t)n * with_hist <= kMaxSmem) {
+      L.nslots = n; L.hist_global = 0; L.slot_bytes = with_hist; break;
+    }
+    if (fixed + (size_t)n * head <= kMaxSmem) {
+      L.nslots = n; L.hist_global = 1; L.slot_bytes = head; break;
+    }
+  }
+  L.smem_bytes = L.nslots ? fixed + (size_t)L.nslots * L.slot_bytes : 0;
+  return L;
 }
-size_t sampler_smem_bytes(uint32_t K) { return sampler_smem_bytes_n(K, std::max<uint32_t>(1u, sampler_slots(K))); }
+uint32_t sampler_slots(uint32_t K) { return sampler_layout(K).nslots; }
+size_t sampler_smem_bytes(uint32_t K) { return sampler_layout(K).smem_bytes; }
 size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
 static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
+uint32_t sampler_grid_size() { return sampler_grid(); }
 
 size_t word_prep_smem_bytes(uint32_t K) { return (size_t)kWpWarps * ((K + 31) / 32) * 32 * 8; }  // row per warp
 

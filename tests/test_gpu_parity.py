@@ -144,10 +144,10 @@ def test_long_docs_block_tier_and_large_rows(ez, oracle_mod):
     run_one_step_parity(ez, oracle_mod, w, d, 60, 3000, 1000, 4, check_every=2)
 
 
-@pytest.mark.parametrize("K", [5000, 11200])
+@pytest.mark.parametrize("K", [5000, 16384])
 def test_large_K_paths(ez, oracle_mod, K):
-    """K > 4096: bitonic doc-pass tier, 32/64-entry S' segments, one item slot per sampler
-    block (K = 11200 is the largest K this build accepts)."""
+    """K > 4096: bitonic doc-pass tier, 32/64-entry S' segments, thread-per-word word-prep,
+    HBM slot histograms (K = 16384 is the largest K this build accepts)."""
     w, d = planted_corpus_np(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21)
     run_one_step_parity(ez, oracle_mod, w, d, 100, 2000, K, 3, check_every=3)
 
