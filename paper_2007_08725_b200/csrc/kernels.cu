@@ -1489,15 +1489,22 @@ SamplerLayout sampler_layout(uint32_t K) {
   L.ws_bytes = (seg_width(K) == 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   const uint32_t head = slot_head_bytes(Kpad), with_hist = head + 4u * Kpad;
-  for (uint32_t n = kMaxSlots; n >= 1; --n) {
-    if (fixed + (size_t)n * with_hist <= kMaxSmem) {
-      L.nslots = n; L.hist_global = 0; L.slot_bytes = with_hist; break;
+  // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it),
+  // then more slots, then shared-memory histograms
+  const size_t budgets[2] = {(228u * 1024u) / EZLDA_SAMP_MINB - 1024u, kMaxSmem};
+  for (size_t budget : budgets)
+    for (uint32_t n = kMaxSlots; n >= 1; --n) {
+      if (fixed + (size_t)n * with_hist <= budget) {
+        L.nslots = n; L.hist_global = 0; L.slot_bytes = with_hist;
+      } else if (fixed + (size_t)n * head <= budget) {
+        L.nslots = n; L.hist_global = 1; L.slot_bytes = head;
+      } else {
+        continue;
+      }
+      L.smem_bytes = fixed + (size_t)L.nslots * L.slot_bytes;
+      if (n == kMaxSlots || budget == kMaxSmem) return L;
+      break;  // fewer slots than wanted under the per-block budget: try the next budget
     }
-    if (fixed + (size_t)n * head <= kMaxSmem) {
-      L.nslots = n; L.hist_global = 1; L.slot_bytes = head; break;
-    }
-  }
-  L.smem_bytes = L.nslots ? fixed + (size_t)L.nslots * L.slot_bytes : 0;
   return L;
 }
 uint32_t sampler_slots(uint32_t K) { return sampler_layout(K).nslots; }
