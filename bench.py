@@ -160,6 +160,11 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--ref-tokens", type=int, default=150_000, help="oracle sample size per --impl reference step")
     ap.add_argument("--doc-block-kb", type=int, default=0, help="sampler L2 tiling (KiB of D rows per block; 0 = off)")
+    # ablations (NEXT-3): W storage, S_est depth, large-word split, exact fp64 draws
+    ap.add_argument("--w-mode", type=int, default=0, help="0 hybrid W (default), 1 all dense, 2 all sparse")
+    ap.add_argument("--g", type=int, default=2, help="S_est depth g in {1,2,3} (Eq 10)")
+    ap.add_argument("--split", type=int, default=0, help="large-word region size in tokens (0 = 10000)")
+    ap.add_argument("--exact-draws", action="store_true", help="every sampled token on the exact fp64 path")
     ap.add_argument("--ncu-traffic", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
     args = ap.parse_args()
 
@@ -207,9 +212,10 @@ def main():
     stream = torch.cuda.Stream(dev)  # a real stream (handle != 0): the library runs on it, events see it
     torch.cuda.set_stream(stream)
     t_create = time.perf_counter()
+    knobs = dict(doc_block_kb=args.doc_block_kb, w_mode=args.w_mode, g=args.g, split_threshold=args.split,
+                 exact_draws=args.exact_draws)
     ez = lda.EzLDA(w, d, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
-                   nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream,
-                   doc_block_kb=args.doc_block_kb)
+                   nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream, **knobs)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t_create
 
@@ -271,7 +277,9 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}-shaped synthetic LDA", "docs": cfg.n_docs, "V": cfg.V, "K": cfg.K,
                    "tokens": N_global, "mean_doc_len": cfg.mean_len, "doc_len_sigma": cfg.sigma,
-                   "alpha": cfg.alpha, "beta": cfg.beta, "g": 2, "iterations_timed": [args.warmup + 1,
+                   "alpha": cfg.alpha, "beta": cfg.beta, "g": args.g, "w_mode": args.w_mode,
+                   "split_threshold": args.split or 10000, "exact_draws": bool(args.exact_draws),
+                   "iterations_timed": [args.warmup + 1,
                                                                                      args.warmup + args.steps],
                    "parallelism": f"doc-partitioned x{world}", "l2": "inputs exceed L2 (corpus state "
                    f">{(N_global * 12) >> 30} GiB vs 126 MB L2); no flush"},
@@ -302,8 +310,7 @@ def main():
             dist.barrier()
         te = time.perf_counter()
         ez2 = lda.EzLDA(hw, hd, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
-                        nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream,
-                   doc_block_kb=args.doc_block_kb)
+                        nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream, **knobs)
         ez2.iterate(args.warmup + args.steps)
         ez2.topics(out=hz)
         torch.cuda.synchronize()
