@@ -553,14 +553,17 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   const uint32_t split = o.split_threshold ? o.split_threshold : 10000u;
   EZ_ALLOC(h, ihead, uint32_t, R);
   // L2 doc windows of doc_block_kb KiB of D rows (0 = 32 MiB): the items of hot words (at
-  // least 256 tokens per window on average) are cut at window boundaries and run
+  // least EZLDA_WIN_TOK tokens per window on average) are cut at window boundaries and run
   // window-major, heavy first -- every D row of the window is then read by many items
   // while it is L2 resident; the other words' items (too few runs per window to amortise
   // the staged What' row) run uncut after them
   const uint64_t blk_kb = o.doc_block_kb ? o.doc_block_kb : 32768ull;
   const uint32_t blk_words = (uint32_t)std::min<uint64_t>(blk_kb * 256ull, 0xFFFFFFFFull);
   const uint64_t nwin = (h->Dwords + blk_words - 1) / blk_words;
-  const uint32_t cut_min = (uint32_t)std::min<uint64_t>(256ull * nwin, 0xFFFFFFFFull);
+#ifndef EZLDA_WIN_TOK
+#define EZLDA_WIN_TOK 1024  // window-cut only words with >= 1024 tokens per D window on average (A/B: 256 .. 16384)
+#endif
+  const uint32_t cut_min = (uint32_t)std::min<uint64_t>((uint64_t)EZLDA_WIN_TOK * nwin, 0xFFFFFFFFull);
   h->cut_min = cut_min;
   k_item_heads<<<blocks(R), 256, 0, s>>>(vs, wrun, tokpre, run_dbase, R, h->Vd, split, blk_words, cut_min, ihead);
   EZ_ALLOC(h, r_iota, uint32_t, R);
