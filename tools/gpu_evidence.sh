@@ -15,3 +15,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/launches_${tag}.log 2>&1; tail -1 gpurun_out/launches_${tag}.log
 bash tools/gpu_prof.sh pubmed ${tag} k_sampler 3
 bash tools/gpu_prof.sh pubmed ${tag}doc k_doc_hist 3
+timeout 600 python tools/curve.py --config pubmed --iters 200 --llpt-every 20 --csv gpurun_out/curve_pubmed_${tag}.csv 2>&1 | tail -1
+timeout 600 python tools/curve.py --config nytimes --iters 200 --llpt-every 20 --csv gpurun_out/curve_nytimes_${tag}.csv 2>&1 | tail -1
