@@ -862,6 +862,13 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t nbefore = __popc(__ballot_sync(kFull, lane < nb && first < B0));
     return nbefore + __popc(bits & (0xFFFFFFFFu >> (31u - lane))) - 1u;
   };
+  // the z^i markers of D's first round are requested now, hidden behind phase B
+  uint32_t zpre = 0;
+  {
+    const uint32_t slot = slot_of(0u, tofs);
+    const uint32_t j = __shfl_sync(kFull, j0, slot) + (lane - __shfl_sync(kFull, tofs, slot));
+    if (lane < ntb) zpre = nxt.z[j];
+  }
   // ---- B: lane per segment (kSegW entries, 16 = two 32-byte sectors); consecutive lanes
   //      read consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the
   //      word's fixed-point What' row), combined by a segmented warp scan (+ carry across
@@ -930,7 +937,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (i >= ntb) continue;
     const uint32_t j = s_j0 + (i - s_tofs);
     const uint32_t* E = d.D + s_ebase;
-    const uint32_t zm = nxt.z[j];
+    const uint32_t zm = B0 ? (uint32_t)nxt.z[j] : zpre;
     uint32_t C1;
     if (d.zmark) {
       if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
