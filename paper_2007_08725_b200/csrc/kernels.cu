@@ -1302,25 +1302,42 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     RunCounters rc{0, 0, 0, 0, 0};
     uint32_t qn = 0;
     bool exhausted = false;
+    bool pf_ok = false;  // a claimed run group (pf_rb) whose flag words (pf_fw) are in flight
+    uint32_t pf_rb = 0, pf_fw = 0;
     while (true) {
-      // refill the queue with flagged runs (warp-uniform control flow throughout)
+      // refill the queue with flagged runs (warp-uniform control flow throughout); the
+      // next group of 32 runs is claimed and its flag words requested one refill ahead
       while (qn < 32 && !exhausted) {
-        uint32_t grp = 0;
-        if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
-        grp = __shfl_sync(kFull, grp, 0);
-        const uint32_t rb = r0 + grp * 32u;
+        uint32_t rb, fw;
+        if (pf_ok) {
+          rb = pf_rb;
+          fw = pf_fw;
+          pf_ok = false;
+        } else {
+          uint32_t grp = 0;
+          if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
+          rb = r0 + __shfl_sync(kFull, grp, 0) * 32u;
+          fw = (rb + lane < r1) ? d.flags[(rb + lane) >> 5] : 0u;
+        }
         if (rb >= r1) {
           exhausted = true;
           break;
         }
         const uint32_t r = rb + lane;
-        const bool act = (r < r1) && ((d.flags[r >> 5] >> (r & 31u)) & 1u);
+        const bool act = (r < r1) && ((fw >> (r & 31u)) & 1u);
         const uint32_t m = __ballot_sync(kFull, act);
         if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
         qn += __popc(m);
         __syncwarp();
       }
       if (qn == 0) break;
+      if (!exhausted && !pf_ok) {
+        uint32_t grp = 0;
+        if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
+        pf_rb = r0 + __shfl_sync(kFull, grp, 0) * 32u;
+        pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
+        pf_ok = true;
+      }
       uint32_t nb;
       switch (d.segw) {
         case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
