@@ -306,11 +306,15 @@ def main():
         del w, d
         torch.cuda.empty_cache()
         torch.cuda.synchronize()
-        if world > 1:
+        nccl_id2 = None
+        if world > 1:  # a ncclUniqueId bootstraps one communicator only: fresh id for this instance
+            obj = [lda.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id2 = obj[0]
             dist.barrier()
         te = time.perf_counter()
         ez2 = lda.EzLDA(hw, hd, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
-                        nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream, **knobs)
+                        nccl_id=nccl_id2, token_base=t0, stream=stream.cuda_stream, **knobs)
         ez2.iterate(args.warmup + args.steps)
         ez2.topics(out=hz)
         torch.cuda.synchronize()
