@@ -78,8 +78,12 @@ typedef struct {
   uint32_t doc_block_kb;     /* L2 tiling: cut hot-word sampler items at doc windows of     */
                              /* this many KiB of D rows, run them window-major;            */
                              /* 0 -> 32768 (32 MiB); 0xFFFFFFFF -> one window (off)        */
-  uint32_t exact_draws;      /* 1: skip the fp32 fast path, draw every sampled token in fp64 */
-                             /* (identical topics by construction; test / ablation knob)   */
+  uint32_t exact_draws;      /* 1: skip the fixed-point fast path, draw every sampled token */
+                             /* in fp64 (identical topics by construction; test knob)      */
+  uint32_t pad0;
+  uint64_t local_group;      /* test hook, world > 1: nonzero key = the ranks are handles of */
+                             /* THIS process on one device (one host thread per rank); the  */
+                             /* W / n_k merge is an in-process device sum instead of NCCL   */
 } ezlda_options;
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL

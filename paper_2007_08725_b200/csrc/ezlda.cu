@@ -14,7 +14,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <cub/cub.cuh>
+#include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -204,6 +207,7 @@ inline unsigned blocks(uint64_t n, unsigned t = 256) { return (unsigned)((n + t 
 // the handle
 // ----------------------------------------------------------------------------
 struct ezlda {
+  void* lgroup = nullptr;  // LocalGroup* of the in-process rank group (options.local_group), else NCCL
   Dev dev{};
   Buf buf[2]{};
   int cur = 0;
@@ -309,8 +313,89 @@ ezlda_status cub_call(ezlda* h, F f) {
   return EZLDA_OK;
 }
 
+// ---- in-process rank group (options.local_group != 0; test hook): the ranks are handles of
+// one process on one device, each driven by its own host thread; the all-reduce is a sum of
+// the ranks' device buffers in rank order (integer sums are exact, so W is bit-identical to
+// the NCCL path).  Everything else of the multi-rank path (relabelling from global counts,
+// all-dense W, token bases, doc shards) runs unchanged, so it can be tested on one GPU.
+struct LocalGroup {
+  std::mutex m;
+  std::condition_variable cv;
+  int world = 0, arrived = 0, left = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> bufs;
+};
+std::mutex g_groups_m;
+std::map<uint64_t, LocalGroup*> g_groups;
+
+LocalGroup* local_group(uint64_t key, int world) {
+  std::lock_guard<std::mutex> lk(g_groups_m);
+  LocalGroup*& g = g_groups[key];
+  if (!g) {
+    g = new LocalGroup();
+    g->world = world;
+    g->bufs.assign(world, nullptr);
+  }
+  return g;
+}
+
+template <typename T>
+__global__ void k_sum_ranks(const T* const* src, int n, size_t count, T* dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    T acc = src[0][i];
+    for (int r = 1; r < n; ++r) acc = acc + src[r][i];
+    dst[i] = acc;
+  }
+}
+
+// barrier of the group; phase = number of completed barriers of this handle
+void group_barrier(LocalGroup* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  const uint64_t my = g->gen;
+  if (++g->arrived == g->world) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->gen != my; });
+  }
+}
+
+ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
+  LocalGroup* g = static_cast<LocalGroup*>(h->lgroup);
+  const size_t esz = (dt == ncclInt32) ? 4 : 8;
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  {
+    std::lock_guard<std::mutex> lk(g->m);
+    g->bufs[h->rank] = buf;
+  }
+  group_barrier(g);  // every rank's buffer is final and registered
+  void* tmp = nullptr;
+  EZ_CUDA(h, cudaMalloc(&tmp, count * esz + sizeof(void*) * g->world));
+  const void** d_src = reinterpret_cast<const void**>(static_cast<char*>(tmp) + count * esz);
+  EZ_CUDA(h, cudaMemcpyAsync(d_src, g->bufs.data(), sizeof(void*) * g->world, cudaMemcpyHostToDevice, h->stream));
+  const unsigned nb = (unsigned)std::min<size_t>((count + 255) / 256, 4096);
+  if (dt == ncclInt32)
+    k_sum_ranks<int32_t><<<nb, 256, 0, h->stream>>>(reinterpret_cast<const int32_t* const*>(d_src), g->world, count,
+                                                     static_cast<int32_t*>(tmp));
+  else if (dt == ncclUint64)
+    k_sum_ranks<unsigned long long><<<nb, 256, 0, h->stream>>>(
+        reinterpret_cast<const unsigned long long* const*>(d_src), g->world, count,
+        static_cast<unsigned long long*>(tmp));
+  else
+    k_sum_ranks<double><<<nb, 256, 0, h->stream>>>(reinterpret_cast<const double* const*>(d_src), g->world, count,
+                                                   static_cast<double*>(tmp));
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  group_barrier(g);  // every rank has read every buffer
+  EZ_CUDA(h, cudaMemcpyAsync(buf, tmp, count * esz, cudaMemcpyDeviceToDevice, h->stream));
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  cudaFree(tmp);
+  return EZLDA_OK;
+}
+
 ezlda_status allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
   if (h->world <= 1 || count == 0) return EZLDA_OK;
+  if (h->lgroup) return local_allreduce(h, buf, count, dt);
   EZ_NCCL(h, nccl().AllReduce(buf, buf, count, dt, ncclSum, h->comm, h->stream));
   return EZLDA_OK;
 }
@@ -835,7 +920,10 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
     }
     h->own_stream = true;
   }
-  if (h->world > 1) {
+  if (h->world > 1 && o.local_group) {
+    if (o.rank < 0 || o.rank >= h->world) st = h->fail(EZLDA_E_INVALID, "local_group needs 0 <= rank < world");
+    else h->lgroup = local_group(o.local_group, h->world);
+  } else if (h->world > 1) {
     if (!o.nccl_unique_id || o.rank < 0 || o.rank >= h->world) {
       st = h->fail(EZLDA_E_INVALID, "world > 1 needs nccl_unique_id and 0 <= rank < world");
     } else if (!nccl().ok) {

@@ -28,7 +28,7 @@ class Options(C.Structure):
         ("split_threshold", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("token_base", C.c_uint64), ("stream", C.c_void_p),
         ("input_on_device", C.c_uint32), ("no_phase_timing", C.c_uint32), ("doc_block_kb", C.c_uint32),
-        ("exact_draws", C.c_uint32),
+        ("exact_draws", C.c_uint32), ("pad0", C.c_uint32), ("local_group", C.c_uint64),
     ]
 
 
@@ -114,7 +114,8 @@ class EzLDA:
                  beta: float = 0.01, seed: int = 1, g: int = 0, w_mode: int = EZLDA_W_HYBRID,
                  dense_threshold: int = 0, split_threshold: int = 0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, token_base: int = 0, stream: int | None = None,
-                 phase_timing: bool = True, doc_block_kb: int = 0, exact_draws: bool = False):
+                 phase_timing: bool = True, doc_block_kb: int = 0, exact_draws: bool = False,
+                 local_group: int = 0):
         L = load()
         self._h = None
         on_dev = bool(getattr(word_ids, "is_cuda", False))
@@ -137,6 +138,7 @@ class EzLDA:
         o.no_phase_timing = 0 if phase_timing else 1
         o.doc_block_kb = doc_block_kb
         o.exact_draws = 1 if exact_draws else 0
+        o.local_group = local_group
         h = C.c_void_p()
         rc = L.ezlda_create(_addr(word_ids), _addr(doc_ids), self.N, self.n_docs, self.V, self.K, self.alpha,
                             self.beta, seed, C.byref(o), C.byref(h))

@@ -288,3 +288,47 @@ def test_invalid_arguments(ez):
     long_doc = np.zeros(70000, np.uint32)
     with pytest.raises(ez.EzLDAError, match="E_RANGE"):
         ez.EzLDA(long_doc, long_doc, 1, 1, 4)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_library_path_one_gpu(ez, world):
+    """The library's multi-rank path (doc shards with token bases, global word counts and
+    relabelling, all-dense W merged every iteration, LLPT reduction) with the ranks as
+    handles of this process on one GPU (options.local_group: the merge is an in-process
+    device sum instead of NCCL).  Concatenated topics, W, n_k and LLPT must equal the
+    single-rank chain bit for bit (P-invariance of the counter-based draws)."""
+    import threading
+
+    w, d = planted_corpus_np(n_docs=600, V=4000, mean_len=90.0, sigma=0.5, seed=17)
+    n_docs, V, K, iters = 600, 4000, 64, 5
+    ref = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED)
+    ref.iterate(iters)
+    z_ref, nk_ref, ll_ref = ref.topics(), ref.n_k(), ref.loglik()
+    W_ref = ez.EzLDA.csr_to_dense(*ref.W_csr(), K)
+    L = np.bincount(d, minlength=n_docs)
+    b = ez.partition_docs(L, world)
+    cum = np.concatenate([[0], np.cumsum(L)])
+    out, errs = {}, []
+
+    def rank_main(r):
+        try:
+            t0, t1 = int(cum[b[r]]), int(cum[b[r + 1]])
+            h = ez.EzLDA(w[t0:t1], d[t0:t1] - b[r], b[r + 1] - b[r], V, K, seed=SAMPLER_SEED, rank=r, world=world,
+                         token_base=t0, local_group=1000 + world)
+            h.iterate(iters)
+            out[r] = (h.topics(), ez.EzLDA.csr_to_dense(*h.W_csr(), K), h.n_k(), h.loglik())
+        except Exception as e:  # surfaced below (the other ranks would wait forever otherwise)
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert not errs, errs
+    z = np.concatenate([out[r][0] for r in range(world)])
+    assert np.array_equal(z, z_ref)
+    for r in range(world):
+        assert np.array_equal(out[r][1], W_ref), r
+        assert np.array_equal(out[r][2], nk_ref), r
+        assert abs(out[r][3] - ll_ref) <= 1e-12 * abs(ll_ref), (out[r][3], ll_ref)
