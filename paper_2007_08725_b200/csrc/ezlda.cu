@@ -416,6 +416,7 @@ void fill_dev(ezlda* h) {
     const ezl::SamplerLayout L = ezl::sampler_layout(h->K);
     d.nslots = L.nslots;
     d.hist_global = L.hist_global;
+    d.hist_bitmap = h->K >= 2048u ? 1u : 0u;
     d.slot_bytes = L.slot_bytes;
     d.ws_bytes = L.ws_bytes;
   }
@@ -776,8 +777,9 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   {  // per-(sampler block, slot) scratch: HBM histograms (large K) and exact Q' tables of
      // warp-staged tail rows
     const size_t n = (size_t)ezl::sampler_grid_size() * d.nslots * d.Kpad;
-    EZ_ALLOC(h, d.hist_scratch, uint32_t, n);
-    EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, n * sizeof(uint32_t), s));
+    const size_t nh = (size_t)ezl::sampler_grid_size() * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
+    EZ_ALLOC(h, d.hist_scratch, uint32_t, nh);
+    EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
     EZ_ALLOC(h, d.qp_scratch, double, n);
   }
   // ---- iteration 0

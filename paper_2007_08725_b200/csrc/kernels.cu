@@ -1034,7 +1034,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     }
     if (hit) rc.hitM += 1;
     nxt.z[j] = (uint16_t)topic;
-    atomicAdd(&hist[topic], 1u);
+    if (d.hist_bitmap) {
+      if (atomicAdd(&hist[topic], 1u) == 0u)  // first token of this topic in the item: mark it
+        atomicOr(&hist[d.Kpad + (topic >> 5)], 1u << (topic & 31u));
+    } else {
+      atomicAdd(&hist[topic], 1u);
+    }
     rc.sampled += 1;
   }
   __syncwarp();
@@ -1191,37 +1196,62 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
 // histogram (dense: atomics; tail: ordered compaction into the packed row), histogram
 // re-zeroed for the slot's next item.
 __device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uint32_t* hist) {
+  // hist[Kpad] counts + bitmap [Kpad / 32] of the topics present: only the marked topics are
+  // visited (O(K/32 + nnz) per item), in ascending order, and re-zeroed
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t v = c.v;
-  if (lane == 0) hist[c.rec.K[0]] += c.ntok - c.sampled;  // skipped tokens stay at K1
-  __syncwarp();
-  if (v < d.Vd) {
-    int32_t* Wrow = nxt.Wd + (size_t)v * d.K;
-    for (uint32_t k = lane; k < d.K; k += 32u) {
-      const uint32_t n = hist[k];
-      if (n) {
-        atomicAdd(&Wrow[k], (int32_t)n);
-        atomicAdd(&nxt.nk[k], (int32_t)n);
-        hist[k] = 0;
-      }
+  uint32_t* bmp = hist + d.Kpad;
+  const uint32_t bw = d.Kpad >> 5;
+  if (lane == 0) {  // skipped tokens stay at K1
+    const uint32_t K1 = c.rec.K[0], n = c.ntok - c.sampled;
+    if (n) {
+      const uint32_t old = hist[K1];
+      hist[K1] = old + n;
+      if (!old && d.hist_bitmap) bmp[K1 >> 5] |= 1u << (K1 & 31u);
     }
-  } else {
-    const uint32_t t = v - d.Vd;
-    uint32_t* out = nxt.Wt + d.tofs[t];
-    uint32_t nz = 0;
+  }
+  __syncwarp();
+  const bool dense = v < d.Vd;
+  int32_t* Wrow = dense ? nxt.Wd + (size_t)v * d.K : nullptr;
+  uint32_t* out = dense ? nullptr : nxt.Wt + d.tofs[v - d.Vd];
+  uint32_t nz = 0;
+  if (!d.hist_bitmap) {  // small K: visit all K counters (no per-token bitmap maintenance)
     for (uint32_t base = 0; base < d.Kpad; base += 32u) {
       const uint32_t k = base + lane;
       const uint32_t n = hist[k];  // zero past K
       const uint32_t m = __ballot_sync(kFull, n != 0);
       if (n) {
-        out[nz + __popc(m & lanemask_lt())] = (k << 16) | n;
+        if (dense) atomicAdd(&Wrow[k], (int32_t)n);
+        else out[nz + __popc(m & lanemask_lt())] = (k << 16) | n;
         atomicAdd(&nxt.nk[k], (int32_t)n);
         hist[k] = 0;
       }
       nz += __popc(m);
     }
-    if (lane == 0) nxt.tnnz[t] = nz;
   }
+  for (uint32_t base = 0; d.hist_bitmap && base < bw; base += 32u) {
+    const uint32_t wi = base + lane;
+    const uint32_t b = (wi < bw) ? bmp[wi] : 0u;
+    const uint32_t cnt = __popc(b);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= (uint32_t)o) incl += y;
+    }
+    uint32_t pos = nz + incl - cnt;
+    for (uint32_t m = b; m; m &= m - 1u) {
+      const uint32_t k = wi * 32u + (__ffs(m) - 1u);
+      const uint32_t n = hist[k];
+      if (dense) atomicAdd(&Wrow[k], (int32_t)n);
+      else out[pos++] = (k << 16) | n;
+      atomicAdd(&nxt.nk[k], (int32_t)n);
+      hist[k] = 0;
+    }
+    if (b) bmp[wi] = 0;
+    nz += __shfl_sync(kFull, incl, 31);
+  }
+  if (!dense && lane == 0) nxt.tnnz[v - d.Vd] = nz;
   if (lane == 0) {
     atomicAdd(&d.ctr->sampled, (unsigned long long)c.sampled);
     atomicAdd(&d.ctr->skip_M, (unsigned long long)c.hitM);
@@ -1261,7 +1291,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
   }
   // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
   auto hist_of = [&](uint32_t sl) -> uint32_t* {
-    return d.hist_global ? d.hist_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad
+    return d.hist_global ? d.hist_scratch + ((size_t)blockIdx.x * nsl + sl) * (d.Kpad + d.Kpad / 32u)
                          : reinterpret_cast<uint32_t*>(slots + sl * sb + slot_head_bytes(d.Kpad));
   };
   auto qps_of = [&](uint32_t sl) -> double* { return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad; };
@@ -1278,7 +1308,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
   if (!d.hist_global)  // (the HBM scratch histograms are zeroed at create and by every epilogue)
     for (uint32_t sl = 0; sl < nsl; ++sl) {
       uint32_t* hist = hist_of(sl);
-      for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+      for (uint32_t k = tid; k < d.Kpad + d.Kpad / 32u; k += blockDim.x) hist[k] = 0;  // counts + bitmap
     }
   __syncthreads();
   if (warp == 0)
@@ -1512,7 +1542,7 @@ SamplerLayout sampler_layout(uint32_t K) {
   const uint32_t Kpad = (K + 31) / 32 * 32;
   L.ws_bytes = (seg_width(K) == 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
-  const uint32_t head = slot_head_bytes(Kpad), with_hist = head + 4u * Kpad;
+  const uint32_t head = slot_head_bytes(Kpad), with_hist = (head + 4u * (Kpad + Kpad / 32u) + 15u) & ~15u;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it),
   // then more slots, then shared-memory histograms
   const size_t budgets[2] = {(228u * 1024u) / EZLDA_SAMP_MINB - 1024u, kMaxSmem};

@@ -54,6 +54,7 @@ struct Dev {
   uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
   uint32_t nslots;   // sampler item slots per block (sampler_layout(K))
   uint32_t hist_global;  // 1: slot histograms in hist_scratch (large K), 0: in shared memory
+  uint32_t hist_bitmap;  // 1 (K >= 2048): item epilogues visit only the topics marked in a bitmap
   uint32_t slot_bytes, ws_bytes;  // sampler shared-memory layout
   uint32_t* hist_scratch;  // [grid * nslots * Kpad] (zero between items)
   double* qp_scratch;      // [grid * nslots * Kpad] exact Q' tables of warp-staged tail rows
