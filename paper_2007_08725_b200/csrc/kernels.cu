@@ -318,49 +318,62 @@ __device__ __forceinline__ void what_reset(const Dev& d, const Buf& cur, uint32_
 }
 
 __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= d.V || d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard
-  WhatCursor c;
-  what_reset(d, cur, v, c);
-  Top4 t;
-  top4_init(t);
-  for (uint32_t k = 0; k < d.K; ++k) top4_insert(t, what_next(d, c, k), k);
-  WordRec r;
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31u;
+  const bool act = v < d.V && d.wtok[v + 1] != d.wtok[v];  // else no token of v in this shard
+  const bool out = act && v < d.Vw;
+  double two_t = 0.0;
+  if (act) {
+    WhatCursor c;
+    what_reset(d, cur, v, c);
+    Top4 t;
+    top4_init(t);
+    for (uint32_t k = 0; k < d.K; ++k) top4_insert(t, what_next(d, c, k), k);
+    WordRec r;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool ok = t.v[i] >= 0.0;
-    r.a[i] = ok ? t.v[i] : 0.0;
-    r.K[i] = ok ? (uint16_t)t.k[i] : (uint16_t)0;
-  }
-  const uint32_t K1 = r.K[0];
-  const bool out = v < d.Vw;
-  WrowPtrs o = wrow_ptrs(d, v);
-  int e = 0;
-  frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
-  const int sh = 32 - e;
-  if (out) {
-    o.sc[0] = ldexp(1.0, -sh);
-    o.sc[1] = ldexp(1.0, sh);
-  }
-  what_reset(d, cur, v, c);
-  double acc = 0.0;
-  for (uint32_t k = 0; k < d.Kpad; ++k) {
-    double w = (k < d.K) ? what_next(d, c, k) : 0.0;
-    if (k == K1) w = 0.0;  // What' (Eq 6): the maximum entry set to 0
-    acc = acc + w;
-    if (k == d.K - 1u) r.Qp = d.alpha * acc;
+    for (int i = 0; i < 4; ++i) {
+      const bool ok = t.v[i] >= 0.0;
+      r.a[i] = ok ? t.v[i] : 0.0;
+      r.K[i] = ok ? (uint16_t)t.k[i] : (uint16_t)0;
+    }
+    const uint32_t K1 = r.K[0];
+    WrowPtrs o = wrow_ptrs(d, v);
+    int e = 0;
+    frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
+    const int sh = 32 - e;
     if (out) {
-      o.m[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
-      o.qp[k] = d.alpha * acc;
+      o.sc[0] = ldexp(1.0, -sh);
+      o.sc[1] = ldexp(1.0, sh);
+    }
+    what_reset(d, cur, v, c);
+    double acc = 0.0;
+    for (uint32_t k = 0; k < d.Kpad; ++k) {
+      double w = (k < d.K) ? what_next(d, c, k) : 0.0;
+      if (k == K1) w = 0.0;  // What' (Eq 6): the maximum entry set to 0
+      acc = acc + w;
+      if (k == d.K - 1u) r.Qp = d.alpha * acc;
+      if (out) {
+        o.m[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
+        o.qp[k] = d.alpha * acc;
+      }
+    }
+    d.rec[v] = r;
+    if (out) {
+      frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
+      two_t = ldexp(1.0, 32 - e);
+      o.sc[2] = ldexp(1.0, e - 32);
+      o.sc[3] = two_t;
     }
   }
-  d.rec[v] = r;
-  if (out) {
-    frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
-    const double two_t = ldexp(1.0, 32 - e);
-    o.sc[2] = ldexp(1.0, e - 32);
-    o.sc[3] = two_t;
-    for (uint32_t k = 0; k < d.Kpad; ++k) o.qfx[k] = __double2uint_rn(fmin(o.qp[k] * two_t, 4294967295.0));
+  // qfx rows of the warp's words, converted cooperatively (coalesced along k)
+  __syncwarp();
+  uint32_t pend = __ballot_sync(kFull, out);
+  while (pend) {
+    const uint32_t src = __ffs(pend) - 1u;
+    pend &= pend - 1u;
+    const uint32_t vw = __shfl_sync(kFull, v, src);
+    const double tt = __shfl_sync(kFull, two_t, src);
+    WrowPtrs o = wrow_ptrs(d, vw);
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(o.qp[k] * tt, 4294967295.0));
   }
 }
 
