@@ -852,7 +852,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t y = __shfl_up_sync(kFull, sincl, o);
     if (lane >= (uint32_t)o) sincl += y;
   }
-  const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kSegCap));  // >= 1
+  constexpr uint32_t kCap = (kSegW == 8u) ? 2u * kSegCap : kSegCap;  // segments per batch
+  const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));  // >= 1
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
   const uint32_t soff = sincl - nseg;
   tincl = (lane < nb) ? len : 0u;
@@ -900,14 +901,20 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t* p = d.D + s_ebase + e0;
     unsigned long long acc = 0ull, acc8 = 0ull;
     if (g < T) {
-#pragma unroll
-      for (uint32_t b = 0; b < kSegW; b += 16u) {
-        uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
-        if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
-        if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
+      if (kSegW == 8u) {  // one sector per lane and round (fewer live registers)
+        uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa;
+        if (e0 < s_nnz) ldg256(p, qa, qb);
         acc = sector_mac(acc, qa, qb, row_s);
-        if (kSec) acc8 = acc;
-        acc = sector_mac(acc, qc, qd, row_s);
+      } else {
+#pragma unroll
+        for (uint32_t b = 0; b < kSegW; b += 16u) {
+          uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
+          if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
+          if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
+          acc = sector_mac(acc, qa, qb, row_s);
+          if (kSec) acc8 = acc;
+          acc = sector_mac(acc, qc, qd, row_s);
+        }
       }
     }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
@@ -991,7 +998,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         }
         const unsigned long long base = (a > c0) ? ws.P[a - 1u] : 0ull;
         unsigned long long pb = base, pa = base;  // prefixes before / after the candidate
-        if (kSec) {  // one sector (8 entries; zero padding past nnz) from registers
+        if (kSec || kSegW == 8u) {  // one sector (8 entries; zero padding past nnz) from registers
           uint4 qa, qb;
           ldg256(E + (a - c0) * 8u, qa, qb);
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -1276,7 +1283,7 @@ __device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uin
 }
 
 #ifndef EZLDA_SAMP_WARPS
-#define EZLDA_SAMP_WARPS 12
+#define EZLDA_SAMP_WARPS 14
 #endif
 constexpr int kSampWarpsP = EZLDA_SAMP_WARPS;
 
@@ -1288,6 +1295,8 @@ __host__ __device__ __forceinline__ uint32_t sampler_ctl_bytes() {
 #define EZLDA_SAMP_MINB 2  // resident sampler blocks per SM the register allocation must allow
 #endif
 
+// one kernel per S' segment width: each gets the register allocation of its own path only
+template <uint32_t kSegW>
 __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter,
                                                                   uint32_t n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1381,14 +1390,8 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
-      uint32_t nb;
-      switch (d.segw) {
-        case 16u: nb = sample_batch<16u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
-        case 32u: nb = sample_batch<32u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
-        case 64u: nb = sample_batch<64u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
-        case 128u: nb = sample_batch<128u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
-        default: nb = sample_batch<256u>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc); break;
-      }
+      const uint32_t nb = sample_batch<kSegW>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc);
+
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
       const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
@@ -1541,9 +1544,12 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
 uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32 + 4u; }  // m | qfx | scales | QP (doubles)
-uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= 16 with K <= kSegCap segw
-  uint32_t w = 16u;
-  while (w * kSegCap < K) w <<= 1;
+#ifndef EZLDA_SEG_MIN
+#define EZLDA_SEG_MIN 16
+#endif
+uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= EZLDA_SEG_MIN, K <= kSegCap segw
+  uint32_t w = EZLDA_SEG_MIN;
+  while (w * (w == 8u ? 2u * kSegCap : kSegCap) < K) w <<= 1;
   return w;
 }
 constexpr size_t kMaxSmem = 227u * 1024u;
@@ -1553,7 +1559,7 @@ constexpr size_t kMaxSmem = 227u * 1024u;
 SamplerLayout sampler_layout(uint32_t K) {
   SamplerLayout L{};
   const uint32_t Kpad = (K + 31) / 32 * 32;
-  L.ws_bytes = (seg_width(K) == 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
+  L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   const uint32_t head = slot_head_bytes(Kpad), with_hist = (head + 4u * (Kpad + Kpad / 32u) + 15u) & ~15u;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it),
@@ -1580,6 +1586,16 @@ size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
+static const void* sampler_kernel(uint32_t segw) {
+  switch (segw) {
+    case 8u: return (const void*)k_sampler<8u>;
+    case 16u: return (const void*)k_sampler<16u>;
+    case 32u: return (const void*)k_sampler<32u>;
+    case 64u: return (const void*)k_sampler<64u>;
+    case 128u: return (const void*)k_sampler<128u>;
+    default: return (const void*)k_sampler<256u>;
+  }
+}
 static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
 uint32_t sampler_grid_size() { return sampler_grid(); }
 
@@ -1592,12 +1608,13 @@ cudaError_t configure_kernels(uint32_t K) {
     return e;
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)llpt_smem_bytes(K)))) return e;
-  if ((e = cudaFuncSetAttribute(k_sampler, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
   {
+    const void* ks = sampler_kernel(seg_width(K));
+    if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
     int dev = 0, nsm = 0, nb = 0;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sampler, kSampWarpsP * 32, (size_t)sp))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks, kSampWarpsP * 32, (size_t)sp))) return e;
     if (nb < 1) return cudaErrorInvalidConfiguration;
     g_sampler_grid = (uint32_t)(nsm * nb);
   }
@@ -1655,8 +1672,22 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
   if (count_only)
     k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
-    k_sampler<<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>(
-        d, cur, nxt, iteration, n_items);
+    switch (d.segw) {
+#define EZ_SAMPLER_LAUNCH(W)                                                                                   \
+  case W:                                                                                                      \
+    k_sampler<W><<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>( \
+        d, cur, nxt, iteration, n_items);                                                                      \
+    break;
+      EZ_SAMPLER_LAUNCH(8u)
+      EZ_SAMPLER_LAUNCH(16u)
+      EZ_SAMPLER_LAUNCH(32u)
+      EZ_SAMPLER_LAUNCH(64u)
+      EZ_SAMPLER_LAUNCH(128u)
+      default:
+        k_sampler<256u><<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>(
+            d, cur, nxt, iteration, n_items);
+#undef EZ_SAMPLER_LAUNCH
+    }
 }
 
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {
