@@ -116,7 +116,7 @@ typedef struct {
   double model_bytes_sample; /* ... of the sampler kernel alone                            */
   double model_bytes_docpass;/* ... of the doc-pass kernels                                */
   uint64_t kernel_launches;  /* library kernels launched by the iteration                  */
-  uint64_t exact_redraws;    /* sampled tokens redrawn on the exact fp64 path (fp32 decision
+  uint64_t exact_redraws;    /* sampled tokens redrawn on the exact fp64 path (fixed-point decision
                                 not certified by its error margin)      */
 } ezlda_iter_stats;
 

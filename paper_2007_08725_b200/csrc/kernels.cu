@@ -3,15 +3,16 @@
 // Per iteration i (snapshot semantics):
 //   k_den        den_k = n_k + V beta, What of absent pairs beta / den_k        (Eq 1-2)
 //   k_word_prep  per word: What row, top-4 (K1..K4, a1..a4), Q'                  (P:546 step 1)
-//   k_doc_warp / k_doc_block
-//                per doc: D row rebuilt from z^{i-1} (sort + run-length encode),
-//                C_j lookups, MPT skip test; skipped tokens get K1, runs with a
-//                failing token are flagged                                       (P:546 steps 2-3)
-//   k_sampler    per work item (word, run range): stage What'[v] in shared memory,
-//                for each flagged (doc, word) run read the D row once, build S'
-//                with a warp scan, draw every failing token of the run with the
-//                [M | S' | Q'] layout, then rebuild W and n_k from the item's
-//                histogram (skipped tokens count at K1)                         (P:546 steps 4-6,
+//   k_doc_hist / k_doc_warp / k_doc_block
+//                per doc: D row rebuilt from z^{i-1} (histogram + bitmap, or sort +
+//                run-length encode), C_j lookups, MPT skip test; skipped tokens get
+//                K1, failing tokens a marker carrying C1, their runs are flagged  (P:546 steps 2-3)
+//   k_sampler    persistent, per work item (word, run range): stage the word's
+//                fixed-point What' row in shared memory, for each flagged (doc, word)
+//                run read the D row once, build S' (exact integers, warp scan), draw
+//                every failing token of the run with the [M | S' | Q'] layout
+//                (certified or redrawn exactly), then rebuild W and n_k from the
+//                item's histogram (skipped tokens count at K1)                  (P:546 steps 4-6,
 //                                                                                  P:822-846)
 #include <algorithm>
 #include <cstdio>
@@ -645,33 +646,32 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
 }
 
 // ---------------------------------------------------------------------------------
-// H5+H6: the residual three-branch sampler + W/n_k rebuild (one block per item).
+// H5+H6: the residual three-branch sampler + W/n_k rebuild.
 // ---------------------------------------------------------------------------------
 //
-// A block owns one work item (word v, a range of its (doc, word) runs).  What'[v] (Eq 6,
-// the K1 entry zeroed) and its chunk prefix CP are staged in shared memory: dense words
-// with ONE TMA bulk copy (cp.async.bulk + mbarrier) of the row word-prep wrote, tail words
-// from beta / den_k plus the word's packed nonzeros.  Warps take groups of 32 runs from an
-// in-block cursor, queue the flagged ones (a token of the run failed the doc pass's MPT
-// test) and process them in batches (P:546 steps 4-6):
+// Work item = (word v, a range of its (doc, word) runs).  The item's fixed-point What' row
+// m_v (Eq 6, K1 entry 0), the fixed-point Q' prefix table and their scales are staged in a
+// shared-memory slot with ONE TMA bulk copy (cp.async.bulk + mbarrier) of the word's wrow
+// head (tail rows word-prep did not precompute are staged by a warp).  Persistent blocks
+// own two slots and pipeline items through them (k_sampler below).  Warps take groups of
+// 32 runs from the item's cursor, queue the flagged ones (a token of the run failed the doc
+// pass's MPT test) and process them in batches (P:546 steps 4-6):
 //
-//  A (lane per run)      run table + D-row header; the row is cut into segments of segw
-//                        entries (8 = one 32-byte sector); a batch admits runs while the
-//                        segment total fits kSegCap;
-//  B (lane per segment)  all 32 lanes busy; consecutive lanes read consecutive sectors of
-//                        a row (coalesced): partial[s] = sequential sum over the segment
-//                        of D[d][k] What'[v][k] in ascending topic order; C1..C3 =
-//                        D[d][K1..K3] are picked up by the lane whose segment holds K_j;
-//  C (lane per run)      P[s] = P[s-1] + partial[s] sequentially over the run's segments,
-//                        S' = P[last]; M (Eq 8), the MPT threshold (Eq 10), Z = M + S' + Q';
-//  D (lane per token)    u (Philox), MPT retest (the doc pass already wrote K1 for skipped
-//                        tokens), x = u Z lands in [M | S' | Q']; S' descent: the first
-//                        segment with P[s] > y (binary search), then the walk
-//                        P[s-1] + (sequential sum inside the segment) -- the same prefix
-//                        definition, so the walk ends exactly at P[s]; Q' descent: binary
-//                        search over CP, then one 32-topic chunk.
-// The S' prefix is a two-level (segment, entry) sum, like the Q' prefix: it differs from
-// the oracle's single sequential sum by rounding only.
+//  A (lane per run)      run table + D-row header; the row is cut into segments of kSegW
+//                        entries (16 = two 32-byte sectors); a batch admits runs while
+//                        the segment total fits the checkpoint array;
+//  B (lane per segment)  consecutive lanes read consecutive sectors of a row (coalesced)
+//                        and accumulate the exact integer products D[d][k] m_v[k]
+//                        (IMAD.WIDE); a segmented warp scan (+ carry across rounds) turns
+//                        segment sums into run prefixes, stored as checkpoints (two per
+//                        16-entry segment); S' = the run's last checkpoint;
+//  D (lane per token)    C1 from the doc pass's z marker, M (Eq 8), Philox u, Z = (M + S')
+//                        + Q', x = u Z in [M | S' | Q']; S' descent: binary search over the
+//                        checkpoints, then a walk of one sector from registers; Q' descent:
+//                        binary search over the fixed-point prefix table.  Each decision
+//                        is certified against the fixed-point error bound or the token is
+//                        redrawn by exact_draw with the oracle's fp64 operations, so the
+//                        topics equal the oracle's.
 struct RunCounters {
   uint32_t sampled, hitM, runs, words, exact;
 };
@@ -772,7 +772,7 @@ __device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint3
 
 // The oracle's per-token draw in fp64 with its summation orders:
 // S' = ascending sequential sum over the row's topics != K1 of D[d][k] What[v][k], Z = (M +
-// S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fp32 fast
+// S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fast
 // path could not certify its decision.
 __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, const uint32_t* E,
                                uint32_t nnz, double M, double u, const double* QP, bool& hitM) {
@@ -817,14 +817,14 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 }
 
 // One batch of flagged runs (warp-uniform control flow).  Returns the number of queue
-// entries consumed.  kSegW: entries per segment (multiple of 16); the per-run state lives
-// in the registers of the run's lane and is fetched by shuffles.
+// entries consumed.  kSegW: entries per segment (8, or a power of two >= 16); the per-run
+// state lives in the registers of the run's lane and is fetched by shuffles.
 //
-// Precision: the S' sums use the fp32 copy of What' (half the shared-memory gather
-// traffic) with fp32 FMA accumulation.  Every decision of the fast path (x vs M, x vs
-// M + S', the S' and Q' descents) is taken only if it holds with a margin that bounds the
-// fp32 error (relative (nnz + 16) 2^-23 of S', far above fp64 rounding); otherwise the token
-// is redrawn by exact_draw.  Either way the topic equals the oracle's fp64 decision.
+// Precision: the S' sums are exact 64-bit integer sums of counts times the word's
+// fixed-point What' row (m = rint(What' 2^s), |m 2^-s - What'| <= 2^-s).  Every decision
+// of the fast path (x vs M, x vs M + S', the S' and Q' descents) is taken only if it holds
+// with a margin bounding that error (2 L_d 2^-s + 4e-15 Z); otherwise the token is redrawn
+// by exact_draw.  Either way the topic equals the oracle's fp64 decision.
 template <uint32_t kSegW>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
                                                  uint32_t v, uint32_t row_s, const uint32_t* qfx, const double* scl,

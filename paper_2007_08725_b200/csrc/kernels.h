@@ -12,7 +12,7 @@
 //     whole sectors without masking):
 //     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+8+i] = (topic << 18) | count
 //     sorted by topic (packed CSR; rebuilt every iteration)
-//   word-major runs r in [0, R) (runs of word v contiguous, ordered by doc length desc):
+//   word-major runs r in [0, R) (runs of word v contiguous, docs ascending):
 //     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
 //   flags[R/32] u32: run r holds a token that failed the MPT skip test (L2 resident)
 //   W: dense rows int32 [Vd x K] for words v < Vd, packed sparse tail rows (capacity
