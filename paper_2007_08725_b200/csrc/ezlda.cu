@@ -416,6 +416,7 @@ void fill_dev(ezlda* h) {
     const ezl::SamplerLayout L = ezl::sampler_layout(h->K);
     d.nslots = L.nslots;
     d.hist_global = L.hist_global;
+    d.qfx_global = L.qfx_global;
     d.hist_bitmap = h->K >= 2048u ? 1u : 0u;
     d.slot_bytes = L.slot_bytes;
     d.ws_bytes = L.ws_bytes;
@@ -780,7 +781,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     const size_t nh = (size_t)ezl::sampler_grid_size() * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
     EZ_ALLOC(h, d.hist_scratch, uint32_t, nh);
     EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
-    EZ_ALLOC(h, d.qp_scratch, double, n);
+    EZ_ALLOC(h, d.qp_scratch, double, n + n / 2);  // QP f64 + qfx u32 per slot
   }
   // ---- iteration 0
   h->cur = 0;

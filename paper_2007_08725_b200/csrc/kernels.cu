@@ -154,9 +154,9 @@ __global__ void k_den(Dev d, Buf cur) {
   }
 }
 
-// wrow record of word v (u32 m | u32 qfx | f64 scales {2^-s, 2^s, 2^-t, 2^t} | f64 QP):
-// the first three parts are one bulk copy into a sampler slot; QP (exact) stays in HBM for
-// the exact redraws.
+// wrow record of word v (u32 m | f64 scales {2^-s, 2^s, 2^-t, 2^t} | u32 qfx | f64 QP): the
+// head (m | scales, plus qfx unless d.qfx_global) is one bulk copy into a sampler slot; QP
+// (exact) stays in HBM for the exact redraws.
 struct WrowPtrs {
   uint32_t* m;
   uint32_t* qfx;
@@ -167,9 +167,9 @@ __device__ __forceinline__ WrowPtrs wrow_ptrs(const Dev& d, uint32_t v) {
   double* b = d.wrow + (size_t)v * d.rs;
   WrowPtrs o;
   o.m = reinterpret_cast<uint32_t*>(b);
-  o.qfx = o.m + d.Kpad;
-  o.sc = b + d.Kpad;
-  o.qp = o.sc + 4;
+  o.sc = b + d.Kpad / 2u;
+  o.qfx = reinterpret_cast<uint32_t*>(o.sc + 4);
+  o.qp = b + d.Kpad + 4u;
   return o;
 }
 
@@ -825,7 +825,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 // of the fast path (x vs M, x vs M + S', the S' and Q' descents) is taken only if it holds
 // with a margin bounding that error (2 L_d 2^-s + 4e-15 Z); otherwise the token is redrawn
 // by exact_draw.  Either way the topic equals the oracle's fp64 decision.
-template <uint32_t kSegW>
+template <uint32_t kSegW, bool kQG>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
                                                  uint32_t v, uint32_t row_s, const uint32_t* qfx, const double* scl,
                                                  const double* const* qpp, uint32_t* hist, WarpScratch& ws,
@@ -1038,12 +1038,14 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           const double inv_t = scl[2];
           const uint32_t Yq = (uint32_t)fmin(y * scl[3], 4294967295.0);  // past the end: uncertified
           uint32_t a = 0, b = d.Kpad - 1u;
+          // the table is in the slot (shared memory) or, for large K (kQG), in HBM
+          auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldg(qfx + i) : qfx[i]; };
           while (a < b) {
             const uint32_t mid = (a + b) >> 1;
-            if (qfx[mid] > Yq) b = mid; else a = mid + 1u;
+            if (qv(mid) > Yq) b = mid; else a = mid + 1u;
           }
           const double mq = mg + inv_t;
-          const double qa = (double)qfx[a] * inv_t, qp = a ? (double)qfx[a - 1u] * inv_t : 0.0;
+          const double qa = (double)qv(a) * inv_t, qp = a ? (double)qv(a - 1u) * inv_t : 0.0;
           if (a != K1 && a < d.K && qa - y > mq && y - qp > mq) topic = a;
         }
       }
@@ -1089,7 +1091,8 @@ struct __align__(16) SlotCtl {
   uint32_t cursor, done;
   uint32_t sampled, hitM, runs, words, exact;
   uint32_t state;  // block item number held by the slot (| kExit: no item left)
-  const double* qp;  // exact Q' prefix table of the item's word (HBM)
+  const double* qp;    // exact Q' prefix table of the item's word (HBM)
+  const uint32_t* qfx; // fixed-point Q' prefix table (slot shared memory, or HBM if d.qfx_global)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t* p) {
@@ -1106,7 +1109,9 @@ __device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
 
 // per-slot dynamic shared memory: m u32 [Kpad] | qfx u32 [Kpad] | scales f64 [4] (one bulk
 // copy of the word's wrow record head) | hist u32 [Kpad] when it fits (else in HBM scratch)
-__host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad) { return 8u * Kpad + 32u; }
+__host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad, uint32_t qfx_global) {
+  return (qfx_global ? 4u : 8u) * Kpad + 32u;  // m | scales [| qfx]
+}
 
 // Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
 // fixed-point What' row, the sequential Q' prefix (the same expressions and order as
@@ -1198,14 +1203,20 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
   }
   if (v < d.Vw) {  // precomputed by word-prep
     if (lane == 0) {
-      c.qp = wrow_ptrs(d, v).qp;
-      bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, slot_head_bytes(d.Kpad), mbar_s);
+      const WrowPtrs o = wrow_ptrs(d, v);
+      c.qp = o.qp;
+      c.qfx = d.qfx_global ? o.qfx : mrow + d.Kpad + 8u;
+      bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs,
+               slot_head_bytes(d.Kpad, d.qfx_global), mbar_s);
     }
   } else {
-    if (lane == 0) c.qp = qp_scratch;
+    uint32_t* qfx = d.qfx_global ? reinterpret_cast<uint32_t*>(qp_scratch + d.Kpad) : mrow + d.Kpad + 8u;
+    if (lane == 0) {
+      c.qp = qp_scratch;
+      c.qfx = qfx;
+    }
     __syncwarp();
-    stage_tail_row_warp(d, cur, v, c.rec, mrow, mrow + d.Kpad, reinterpret_cast<double*>(mrow + 2u * d.Kpad),
-                        qp_scratch);
+    stage_tail_row_warp(d, cur, v, c.rec, mrow, qfx, reinterpret_cast<double*>(mrow + d.Kpad), qp_scratch);
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
   }
   __syncwarp();
@@ -1295,8 +1306,9 @@ __host__ __device__ __forceinline__ uint32_t sampler_ctl_bytes() {
 #define EZLDA_SAMP_MINB 2  // resident sampler blocks per SM the register allocation must allow
 #endif
 
-// one kernel per S' segment width: each gets the register allocation of its own path only
-template <uint32_t kSegW>
+// one kernel per (S' segment width, Q' table placement): each gets the register allocation
+// of its own path only
+template <uint32_t kSegW, bool kQG>
 __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter,
                                                                   uint32_t n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1314,9 +1326,12 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
   // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
   auto hist_of = [&](uint32_t sl) -> uint32_t* {
     return d.hist_global ? d.hist_scratch + ((size_t)blockIdx.x * nsl + sl) * (d.Kpad + d.Kpad / 32u)
-                         : reinterpret_cast<uint32_t*>(slots + sl * sb + slot_head_bytes(d.Kpad));
+                         : reinterpret_cast<uint32_t*>(slots + sl * sb + slot_head_bytes(d.Kpad, d.qfx_global));
   };
-  auto qps_of = [&](uint32_t sl) -> double* { return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad; };
+  // exact QP [Kpad] f64 (+ qfx [Kpad] u32 when d.qfx_global) of a warp-staged tail row
+  auto qps_of = [&](uint32_t sl) -> double* {
+    return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * (d.Kpad + d.Kpad / 2u);
+  };
   const uint32_t nw = blockDim.x >> 5;
   // prologue: barriers, zero histograms, warp 0 arms the first kSlots items
   if (tid == 0) {
@@ -1345,8 +1360,9 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     st = __shfl_sync(kFull, st, 0);
     if (st & kExit) break;
     mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
-    const uint32_t* qfx = reinterpret_cast<const uint32_t*>(slots + sl * sb + 4u * d.Kpad);
-    const double* scl = reinterpret_cast<const double*>(slots + sl * sb + 8u * d.Kpad);
+    // fixed-point Q' table: in the slot right after the scales, or in HBM (kQG, large K)
+    const uint32_t* qfx = kQG ? c.qfx : reinterpret_cast<const uint32_t*>(slots + sl * sb + 4u * d.Kpad + 32u);
+    const double* scl = reinterpret_cast<const double*>(slots + sl * sb + 4u * d.Kpad);
     uint32_t* hist = hist_of(sl);
     const WordRec rec = c.rec;
     const uint32_t v = c.v, r0 = c.r0, r1 = c.r1;
@@ -1390,7 +1406,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
-      const uint32_t nb = sample_batch<kSegW>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc);
+      const uint32_t nb = sample_batch<kSegW, kQG>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc);
 
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
@@ -1561,22 +1577,26 @@ SamplerLayout sampler_layout(uint32_t K) {
   const uint32_t Kpad = (K + 31) / 32 * 32;
   L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
-  const uint32_t head = slot_head_bytes(Kpad), with_hist = (head + 4u * (Kpad + Kpad / 32u) + 15u) & ~15u;
-  // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it),
-  // then more slots, then shared-memory histograms
+  // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it)
+  // with two slots; per budget: histograms and the Q' table in shared memory, else the
+  // histograms in HBM scratch, else also the Q' table in HBM; last resort one slot
   const size_t budgets[2] = {(228u * 1024u) / EZLDA_SAMP_MINB - 1024u, kMaxSmem};
   for (size_t budget : budgets)
     for (uint32_t n = kMaxSlots; n >= 1; --n) {
-      if (fixed + (size_t)n * with_hist <= budget) {
-        L.nslots = n; L.hist_global = 0; L.slot_bytes = with_hist;
-      } else if (fixed + (size_t)n * head <= budget) {
-        L.nslots = n; L.hist_global = 1; L.slot_bytes = head;
-      } else {
-        continue;
+      if (n < kMaxSlots && budget != kMaxSmem) break;
+      for (uint32_t mode = 0; mode < 3; ++mode) {
+        const uint32_t qg = mode == 2 ? 1u : 0u, hg = mode >= 1 ? 1u : 0u;
+        const uint32_t head = slot_head_bytes(Kpad, qg);
+        const uint32_t sb = hg ? head : ((head + 4u * (Kpad + Kpad / 32u) + 15u) & ~15u);
+        if (fixed + (size_t)n * sb <= budget) {
+          L.nslots = n;
+          L.hist_global = hg;
+          L.qfx_global = qg;
+          L.slot_bytes = sb;
+          L.smem_bytes = fixed + (size_t)n * sb;
+          return L;
+        }
       }
-      L.smem_bytes = fixed + (size_t)L.nslots * L.slot_bytes;
-      if (n == kMaxSlots || budget == kMaxSmem) return L;
-      break;  // fewer slots than wanted under the per-block budget: try the next budget
     }
   return L;
 }
@@ -1586,14 +1606,12 @@ size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
-static const void* sampler_kernel(uint32_t segw) {
-  switch (segw) {
-    case 8u: return (const void*)k_sampler<8u>;
-    case 16u: return (const void*)k_sampler<16u>;
-    case 32u: return (const void*)k_sampler<32u>;
-    case 64u: return (const void*)k_sampler<64u>;
-    case 128u: return (const void*)k_sampler<128u>;
-    default: return (const void*)k_sampler<256u>;
+static const void* sampler_kernel(uint32_t segw, uint32_t qg) {
+  switch (segw) {  // K <= 16384: segment widths 8 .. 64
+    case 8u: return qg ? (const void*)k_sampler<8u, true> : (const void*)k_sampler<8u, false>;
+    case 16u: return qg ? (const void*)k_sampler<16u, true> : (const void*)k_sampler<16u, false>;
+    case 32u: return qg ? (const void*)k_sampler<32u, true> : (const void*)k_sampler<32u, false>;
+    default: return qg ? (const void*)k_sampler<64u, true> : (const void*)k_sampler<64u, false>;
   }
 }
 static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
@@ -1609,7 +1627,7 @@ cudaError_t configure_kernels(uint32_t K) {
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)llpt_smem_bytes(K)))) return e;
   {
-    const void* ks = sampler_kernel(seg_width(K));
+    const void* ks = sampler_kernel(seg_width(K), sampler_layout(K).qfx_global);
     if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
     int dev = 0, nsm = 0, nb = 0;
     if ((e = cudaGetDevice(&dev))) return e;
@@ -1672,21 +1690,11 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
   if (count_only)
     k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
-    switch (d.segw) {
-#define EZ_SAMPLER_LAUNCH(W)                                                                                   \
-  case W:                                                                                                      \
-    k_sampler<W><<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>( \
-        d, cur, nxt, iteration, n_items);                                                                      \
-    break;
-      EZ_SAMPLER_LAUNCH(8u)
-      EZ_SAMPLER_LAUNCH(16u)
-      EZ_SAMPLER_LAUNCH(32u)
-      EZ_SAMPLER_LAUNCH(64u)
-      EZ_SAMPLER_LAUNCH(128u)
-      default:
-        k_sampler<256u><<<std::min<uint32_t>(n_items, sampler_grid()), kSampWarpsP * 32, sampler_smem_bytes(d.K), s>>>(
-            d, cur, nxt, iteration, n_items);
-#undef EZ_SAMPLER_LAUNCH
+    {
+      const void* ks = sampler_kernel(d.segw, d.qfx_global);
+      const uint32_t grid = std::min<uint32_t>(n_items, sampler_grid());
+      void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
+      cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);
     }
 }
 

@@ -18,9 +18,9 @@
 //   W: dense rows int32 [Vd x K] for words v < Vd, packed sparse tail rows (capacity
 //     min(c_v, K) at tofs[v-Vd]) with tnnz[v-Vd]; double-buffered with n_k[K].
 //   rec[V] WordRec (48 B): top-4 topics/values and Q' of every word.
-//   wrow[Vw][rs]: per word u32 m[Kpad] (fixed-point What', K1 entry 0) | u32 qfx[Kpad]
-//     (fixed-point Q' prefix) | f64 {2^-s, 2^s, 2^-t, 2^t} | f64 QP[Kpad] (exact Q' prefix)
-//     -- written by word-prep; the head (m | qfx | scales) is bulk-copied (TMA) into a
+//   wrow[Vw][rs]: per word u32 m[Kpad] (fixed-point What', K1 entry 0) | f64 {2^-s, 2^s,
+//     2^-t, 2^t} | u32 qfx[Kpad] (fixed-point Q' prefix) | f64 QP[Kpad] (exact Q' prefix)
+//     -- written by word-prep; the head (m | scales [| qfx]) is bulk-copied (TMA) into a
 //     sampler slot, QP is read by the exact redraws.
 //   items: (word, run range, tokens): the sampler's work list, heavy first.
 #pragma once
@@ -54,10 +54,11 @@ struct Dev {
   uint32_t N, Dn, V, K, Kpad, nch, Vd, geff;
   uint32_t nslots;   // sampler item slots per block (sampler_layout(K))
   uint32_t hist_global;  // 1: slot histograms in hist_scratch (large K), 0: in shared memory
-  uint32_t hist_bitmap;  // 1 (K >= 2048): item epilogues visit only the topics marked in a bitmap
+  uint32_t hist_bitmap;
+  uint32_t qfx_global;   // 1 (large K): the fixed-point Q' table is searched in HBM, not staged  // 1 (K >= 2048): item epilogues visit only the topics marked in a bitmap
   uint32_t slot_bytes, ws_bytes;  // sampler shared-memory layout
   uint32_t* hist_scratch;  // [grid * nslots * Kpad] (zero between items)
-  double* qp_scratch;      // [grid * nslots * Kpad] exact Q' tables of warp-staged tail rows
+  double* qp_scratch;      // [grid * nslots * 1.5 Kpad] exact Q' (+ fixed-point) tables of warp-staged tail rows
   uint32_t exact_all;  // 1: every sampled token takes the exact fp64 path (test/ablation knob)
   uint32_t Vw;     // words v < Vw have their What' | QP row precomputed in wrow (Vd, or V if it fits)
   uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, 0x7FFF)
@@ -117,7 +118,7 @@ void launch_topics_from_input(const uint16_t* in, const uint32_t* perm, uint32_t
 size_t sampler_smem_bytes(uint32_t K);
 uint32_t sampler_slots(uint32_t K);  // pipelined item slots per sampler block (0: K too large)
 struct SamplerLayout {
-  uint32_t nslots, hist_global, slot_bytes, ws_bytes;
+  uint32_t nslots, hist_global, qfx_global, slot_bytes, ws_bytes;
   size_t smem_bytes;
 };
 SamplerLayout sampler_layout(uint32_t K);
