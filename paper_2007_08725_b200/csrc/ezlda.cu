@@ -781,7 +781,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     const size_t nh = (size_t)ezl::sampler_grid_size() * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
     EZ_ALLOC(h, d.hist_scratch, uint32_t, nh);
     EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
-    EZ_ALLOC(h, d.qp_scratch, double, n + n / 2);  // QP f64 + qfx u32 per slot
+    EZ_ALLOC(h, d.qp_scratch, double,
+             (size_t)ezl::sampler_grid_size() * d.nslots * ezl::sampler_qp_scratch_stride(d.Kpad));
   }
   // ---- iteration 0
   h->cur = 0;

@@ -157,9 +157,16 @@ __global__ void k_den(Dev d, Buf cur) {
 // wrow record of word v (u32 m | f64 scales {2^-s, 2^s, 2^-t, 2^t} | u32 qfx | f64 QP): the
 // head (m | scales, plus qfx unless d.qfx_global) is one bulk copy into a sampler slot; QP
 // (exact) stays in HBM for the exact redraws.
+// chunk ends of the fixed-point Q' table: ce[c] = qfx[32 c + 31] (contiguous, so the first
+// half of a Q' search probes one 128-byte line instead of one bank), padded to 16 bytes
+__host__ __device__ __forceinline__ uint32_t ce_words(uint32_t Kpad) { return ((Kpad / 32u) + 3u) & ~3u; }
+// per-slot HBM scratch of a warp-staged tail row, in doubles: QP f64 [Kpad] | qfx u32 [Kpad] | ce
+__host__ __device__ __forceinline__ uint32_t qp_scratch_stride(uint32_t Kpad) { return Kpad + Kpad / 2u + ce_words(Kpad) / 2u; }
+
 struct WrowPtrs {
   uint32_t* m;
   uint32_t* qfx;
+  uint32_t* ce;
   double* sc;
   double* qp;
 };
@@ -169,7 +176,8 @@ __device__ __forceinline__ WrowPtrs wrow_ptrs(const Dev& d, uint32_t v) {
   o.m = reinterpret_cast<uint32_t*>(b);
   o.sc = b + d.Kpad / 2u;
   o.qfx = reinterpret_cast<uint32_t*>(o.sc + 4);
-  o.qp = b + d.Kpad + 4u;
+  o.ce = o.qfx + d.Kpad;
+  o.qp = b + d.Kpad + 4u + ce_words(d.Kpad) / 2u;
   return o;
 }
 
@@ -275,6 +283,8 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
     __syncwarp();
     const double two_t = o.sc[3];
     for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(outq[k] * two_t, 4294967295.0));
+    for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)
+      o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(outq[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
   }
 }
 
@@ -375,6 +385,8 @@ __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
     const double tt = __shfl_sync(kFull, two_t, src);
     WrowPtrs o = wrow_ptrs(d, vw);
     for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(o.qp[k] * tt, 4294967295.0));
+    for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)
+      o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(o.qp[32u * c + 31u] * tt, 4294967295.0)) : 0xFFFFFFFFu;
   }
 }
 
@@ -929,9 +941,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (kSec) {
       unsigned long long excl = __shfl_up_sync(kFull, acc, 1);
       if (lane == rs) excl = cont ? carry : 0ull;
-      if (g < T) {
-        ws.P[2u * g] = excl + acc8;
-        ws.P[2u * g + 1u] = acc;
+      if (g < T) {  // the two checkpoints of a segment are adjacent: one 16-byte store
+        const unsigned long long c0v = excl + acc8;
+        ulonglong2 pr;
+        pr.x = c0v;
+        pr.y = acc;
+        *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
       }
     } else if (g < T) {
       ws.P[g] = acc;
@@ -1040,6 +1055,16 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           uint32_t a = 0, b = d.Kpad - 1u;
           // the table is in the slot (shared memory) or, for large K (kQG), in HBM
           auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldg(qfx + i) : qfx[i]; };
+          if (!kQG) {  // first the 32-topic chunk from the contiguous chunk ends
+            const uint32_t* ce = qfx + d.Kpad;
+            uint32_t ca = 0, cb = d.nch - 1u;
+            while (ca < cb) {
+              const uint32_t mid = (ca + cb) >> 1;
+              if (ce[mid] > Yq) cb = mid; else ca = mid + 1u;
+            }
+            a = 32u * ca;
+            b = a + 31u;
+          }
           while (a < b) {
             const uint32_t mid = (a + b) >> 1;
             if (qv(mid) > Yq) b = mid; else a = mid + 1u;
@@ -1110,7 +1135,7 @@ __device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
 // per-slot dynamic shared memory: m u32 [Kpad] | qfx u32 [Kpad] | scales f64 [4] (one bulk
 // copy of the word's wrow record head) | hist u32 [Kpad] when it fits (else in HBM scratch)
 __host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad, uint32_t qfx_global) {
-  return (qfx_global ? 4u : 8u) * Kpad + 32u;  // m | scales [| qfx]
+  return qfx_global ? 4u * Kpad + 32u : 8u * Kpad + 32u + 4u * ce_words(Kpad);  // m | scales [| qfx | ce]
 }
 
 // Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
@@ -1163,6 +1188,8 @@ __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, co
   const double two_t = ldexp(1.0, 32 - et);
   __syncwarp();
   for (uint32_t k = lane; k < d.Kpad; k += 32u) qfx[k] = __double2uint_rn(fmin(QP[k] * two_t, 4294967295.0));
+  for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)  // chunk ends right after qfx
+    qfx[d.Kpad + c] = (c < d.nch) ? __double2uint_rn(fmin(QP[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
   if (lane == 0) {
     sc[0] = ldexp(1.0, -sh);
     sc[1] = ldexp(1.0, sh);
@@ -1330,7 +1357,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
   };
   // exact QP [Kpad] f64 (+ qfx [Kpad] u32 when d.qfx_global) of a warp-staged tail row
   auto qps_of = [&](uint32_t sl) -> double* {
-    return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * (d.Kpad + d.Kpad / 2u);
+    return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * qp_scratch_stride(d.Kpad);
   };
   const uint32_t nw = blockDim.x >> 5;
   // prologue: barriers, zero histograms, warp 0 arms the first kSlots items
@@ -1559,7 +1586,10 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-uint32_t wrow_stride(uint32_t K) { return 2u * ((K + 31) / 32) * 32 + 4u; }  // m | qfx | scales | QP (doubles)
+uint32_t wrow_stride(uint32_t K) {  // m | scales | qfx | ce | QP (doubles)
+  const uint32_t Kpad = (K + 31) / 32 * 32;
+  return 2u * Kpad + 4u + ce_words(Kpad) / 2u;
+}
 #ifndef EZLDA_SEG_MIN
 #define EZLDA_SEG_MIN 16
 #endif
@@ -1616,6 +1646,7 @@ static const void* sampler_kernel(uint32_t segw, uint32_t qg) {
 }
 static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
 uint32_t sampler_grid_size() { return sampler_grid(); }
+uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
 
 size_t word_prep_smem_bytes(uint32_t K) { return (size_t)kWpWarps * ((K + 31) / 32) * 32 * 8; }  // row per warp
 

@@ -123,6 +123,7 @@ struct SamplerLayout {
 };
 SamplerLayout sampler_layout(uint32_t K);
 uint32_t sampler_grid_size();  // persistent sampler grid (after configure_kernels)
+uint32_t sampler_qp_scratch_stride(uint32_t Kpad);  // doubles per slot of qp_scratch
 uint32_t wrow_stride(uint32_t K);
 uint32_t seg_width(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);
