@@ -307,6 +307,7 @@ struct ezlda_oracle {
   uint64_t* wofs;       /* [V+1] CSR of tokens by word */
   uint64_t* wtok;       /* [N] */
   uint32_t iterations;
+  uint32_t branches;    /* 3 = three-branch sampler (default), 2 = two-branch ESCA */
   uint64_t skip_S, skip_final, branch_hist[4];
 };
 
@@ -369,7 +370,14 @@ int ezlda_oracle_create(const uint32_t* word_ids, const uint32_t* doc_ids, uint6
   /* iteration 0: random initial topics */
   for (uint64_t t = 0; t < n_tokens; ++t) h->z[t] = (uint16_t)ezlda_oracle_init_topic(seed, h->tg[t], K);
   h->iterations = 0;
+  h->branches = 3;
   *out = h;
+  return 0;
+}
+
+int ezlda_oracle_set_sampler(ezlda_oracle* h, uint32_t branches) {
+  if (!h || (branches != 2 && branches != 3)) return 1;
+  h->branches = branches;
   return 0;
 }
 
@@ -449,6 +457,13 @@ int ezlda_oracle_iterate(ezlda_oracle* h, uint32_t n, const int32_t* W_global, c
       for (uint64_t q = h->wofs[v]; q < h->wofs[v + 1]; ++q) {
         const uint64_t t = h->wtok[q];
         const double u = ezlda_oracle_uniform(h->seed, i, h->tg[t]);
+        if (h->branches == 2) { /* two-branch ESCA draw (Fig 2 text, reading #11); no skip test */
+          double S, Q;
+          znew[t] = (uint16_t)ezlda_oracle_draw_two_branch(D + (size_t)h->doc[t] * K, What, K, h->alpha, u,
+                                                           &S, &Q, NULL, NULL, NULL);
+          h->branch_hist[(u <= S / (S + Q)) ? 2 : 3] += 1;
+          continue;
+        }
         ezlda_oracle_draw_detail det;
         token_draw(&rec, P, What, D + (size_t)h->doc[t] * K, K, h->alpha, h->g, u, &det);
         znew[t] = (uint16_t)det.topic;

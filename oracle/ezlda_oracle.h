@@ -89,6 +89,10 @@ uint32_t ezlda_oracle_iterations(const ezlda_oracle* h);
  * W_global/nk_global override the snapshot as in iterate (may be NULL). */
 int ezlda_oracle_what(const ezlda_oracle* h, uint32_t v, const int32_t* W_global, const int32_t* nk_global,
                       double* row);
+/* Sampler of the chain: 3 = three-branch (default), 2 = two-branch ESCA
+ * (ezlda_oracle_draw_two_branch per token, no skip test, Alg P:1481-1507).
+ * last_stats then reports skip_S = skip_final = 0 and branch_hist[2] / [3] = S / Q draws. */
+int ezlda_oracle_set_sampler(ezlda_oracle* h, uint32_t branches);
 /* Run n snapshot iterations.  W_global/nk_global (V*K and K ints) override the W snapshot
  * of the FIRST of them when non-NULL (multi-shard emulation: W is the sum over shards). */
 int ezlda_oracle_iterate(ezlda_oracle* h, uint32_t n, const int32_t* W_global, const int32_t* nk_global);

@@ -68,6 +68,8 @@ def lib():
                                                    C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
                                                    P(C.c_double), P(C.c_double)]
         L.ezlda_oracle_draw_two_branch.restype = C.c_uint32
+        L.ezlda_oracle_set_sampler.argtypes = [C.c_void_p, C.c_uint32]
+        L.ezlda_oracle_set_sampler.restype = C.c_int
         L.ezlda_oracle_inverted_index.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32,
                                                   P(C.c_uint64), P(C.c_uint64)]
         L.ezlda_oracle_create.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32, C.c_uint32,
@@ -162,7 +164,7 @@ class OracleLDA:
     """The plain CPU chain: create / iterate / topics / counts / loglik."""
 
     def __init__(self, word_ids, doc_ids, n_docs: int, V: int, K: int, alpha: float | None = None,
-                 beta: float = 0.01, seed: int = 1, g: int = 2, token_base: int = 0):
+                 beta: float = 0.01, seed: int = 1, g: int = 2, token_base: int = 0, branches: int = 3):
         self.word = np.ascontiguousarray(word_ids, dtype=np.uint32)
         self.doc = np.ascontiguousarray(doc_ids, dtype=np.uint32)
         self.N = len(self.word)
@@ -175,6 +177,8 @@ class OracleLDA:
         if rc:
             raise ValueError(f"ezlda_oracle_create rc={rc}")
         self._h = h
+        if lib().ezlda_oracle_set_sampler(h, branches):
+            raise ValueError("branches must be 2 or 3")
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -155,3 +155,40 @@ def test_shard_emulation_equals_single(oracle_mod, tiny, P):
             s.iterate(1, Wg, ng)
         ref.iterate(1)
         assert np.array_equal(np.concatenate([s.topics() for s in shards]), ref.topics())
+
+
+def test_two_branch_chain_invariants_and_convergence(oracle_mod, tiny):
+    """Two-branch (ESCA) chain mode (Alg P:1481-1507): exact counts, no skipping,
+    every token drawn in the S or Q branch, and the LLPT rises like the three-branch chain's."""
+    w, d = tiny
+    n_docs, V, K = TINY["n_docs"], TINY["V"], 16
+    h = oracle_mod.OracleLDA(w, d, n_docs, V, K, branches=2)
+    h3 = oracle_mod.OracleLDA(w, d, n_docs, V, K)
+    assert np.array_equal(h.topics(), h3.topics())  # same iteration-0 state
+    ll, ll3 = [], []
+    for _ in range(20):
+        h.iterate(1)
+        h3.iterate(1)
+        ll.append(h.loglik(1))
+        ll3.append(h3.loglik(1))
+        st = h.last_stats()
+        assert st["skip_S"] == st["skip_final"] == 0
+        assert st["branch_hist"][0] == st["branch_hist"][1] == 0
+        assert st["branch_hist"][2] + st["branch_hist"][3] == len(w)
+    z = h.topics()
+    D, W, nk = h.counts()
+    Db, Wb = brute_counts(w, d, z, n_docs, V, K)
+    assert np.array_equal(D, Db) and np.array_equal(W, Wb)
+    assert ll[-1] > ll[0] + 0.1
+    # same conditional, different u -> topic maps: different chains, similar likelihood
+    assert not np.array_equal(z, h3.topics())
+    assert abs(np.mean(ll[-5:]) - np.mean(ll3[-5:])) < 0.1 * abs(np.mean(ll3[-5:]))
+
+
+def test_two_branch_K1_all_zero(oracle_mod, tiny):
+    w, d = tiny
+    h = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 1, branches=2)
+    h.iterate(2)
+    assert not h.topics().any()
+    with pytest.raises(ValueError):
+        oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 4, branches=1)

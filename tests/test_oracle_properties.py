@@ -97,3 +97,23 @@ def test_degenerate_K1_and_K2(oracle_mod):
     # doc with every token at K1: S_est = S' = 0
     det = oracle_mod.draw_three_branch([0, 4, 0], [0.1, 0.9, 0.3], 1.0, 2, 0.0)
     assert det["S_est"] == 0.0
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_two_branch_u_measure_equals_conditional(oracle_mod, seed):
+    """The two-branch (ESCA) map of the Fig 2 text (reading #11) samples the
+    same textbook conditional: S branch on [0, S/Z] with u' = uZ, Q branch with u' = (1-u)Z."""
+    rng = np.random.default_rng(5000 + seed)
+    K = int(rng.integers(2, 12))
+    alpha = float(rng.uniform(0.05, 5.0))
+    D, What = random_state(rng, K)
+    G = 20000
+    u = (np.arange(G) + 0.5) / G
+    p = textbook_p(D, What, alpha)
+    topics = np.array([oracle_mod.draw_two_branch(D, What, alpha, float(x))["topic"] for x in u])
+    freq = np.bincount(topics, minlength=K) / G
+    # each topic: one interval in the S branch, one (reversed) in the Q branch
+    np.testing.assert_allclose(freq, p, atol=4.0 / G + 1e-12)
+    # the S branch only ever returns topics present in the doc row
+    r = oracle_mod.draw_two_branch(D, What, alpha, 0.0)
+    assert D[r["topic"]] > 0 or D.sum() == 0
