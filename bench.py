@@ -165,6 +165,8 @@ def main():
     ap.add_argument("--g", type=int, default=2, help="S_est depth g in {1,2,3} (Eq 10)")
     ap.add_argument("--split", type=int, default=0, help="large-word region size in tokens (0 = 10000)")
     ap.add_argument("--exact-draws", action="store_true", help="every sampled token on the exact fp64 path")
+    ap.add_argument("--sampler", type=int, default=3, choices=[2, 3],
+                    help="3: three-branch (default); 2: the paper's two-branch ESCA baseline mode (NEXT-1)")
     ap.add_argument("--ncu-traffic", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
     args = ap.parse_args()
 
@@ -213,7 +215,7 @@ def main():
     torch.cuda.set_stream(stream)
     t_create = time.perf_counter()
     knobs = dict(doc_block_kb=args.doc_block_kb, w_mode=args.w_mode, g=args.g, split_threshold=args.split,
-                 exact_draws=args.exact_draws)
+                 exact_draws=args.exact_draws, sampler=args.sampler)
     ez = lda.EzLDA(w, d, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
                    nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream, **knobs)
     torch.cuda.synchronize()
@@ -271,6 +273,12 @@ def main():
                            "achieved_gbs": S["model_bytes"] / (ms / 1e3) / 1e9,
                            "frac": S["model_bytes"] / (ms / 1e3) / 1e9 / peak}}
 
+    if args.sampler == 2:  # the byte model describes the three-branch kernels
+        roof.update({"achieved": None, "frac": None, "traffic": None, "algorithmic_bytes_per_launch": None,
+                     "kernel": "two-branch draw + W rebuild",
+                     "note": "two-branch baseline mode: no byte model; compare ms_per_step"})
+        roof["whole_step"] = None
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -279,6 +287,7 @@ def main():
                    "tokens": N_global, "mean_doc_len": cfg.mean_len, "doc_len_sigma": cfg.sigma,
                    "alpha": cfg.alpha, "beta": cfg.beta, "g": args.g, "w_mode": args.w_mode,
                    "split_threshold": args.split or 10000, "exact_draws": bool(args.exact_draws),
+                   "sampler": "two-branch (ESCA)" if args.sampler == 2 else "three-branch",
                    "iterations_timed": [args.warmup + 1,
                                                                                      args.warmup + args.steps],
                    "parallelism": f"doc-partitioned x{world}", "l2": "inputs exceed L2 (corpus state "

@@ -80,7 +80,10 @@ typedef struct {
                              /* 0 -> 32768 (32 MiB); 0xFFFFFFFF -> one window (off)        */
   uint32_t exact_draws;      /* 1: skip the fixed-point fast path, draw every sampled token */
                              /* in fp64 (identical topics by construction; test knob)      */
-  uint32_t pad0;
+  uint32_t sampler;          /* 0 or 3: the three-branch sampler; 2: the two-branch */
+                             /* ESCA sampler (Eq 3-4, Alg P:1481-1507) on the same   */
+                             /* D/W rebuild -- the paper's baseline (reading #11 of SURVEY 8c). */
+                             /* Any other value -> EZLDA_E_INVALID.                             */
   uint64_t local_group;      /* test hook, world > 1: nonzero key = the ranks are handles of */
                              /* THIS process on one device (one host thread per rank); the  */
                              /* W / n_k merge is an in-process device sum instead of NCCL   */

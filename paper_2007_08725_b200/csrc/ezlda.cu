@@ -244,6 +244,7 @@ struct ezlda {
   uint64_t slot_counter = 0;
   ezl::Counters* ctr_host = nullptr;  // pinned, kSlots entries
   uint32_t exact_all = 0;             // options.exact_draws
+  uint32_t branches = 3;              // options.sampler (2: two-branch ESCA mode)
   ezlda_iter_stats sum{};
   uint32_t sum_n = 0;
   double* llpt_partial = nullptr;
@@ -422,6 +423,7 @@ void fill_dev(ezlda* h) {
     d.ws_bytes = L.ws_bytes;
   }
   d.exact_all = h->exact_all;
+  d.branches = h->branches;
   d.geff = std::min<uint32_t>(h->g, h->K - 1);
   d.alpha = h->alpha;
   d.beta = h->beta;
@@ -749,8 +751,13 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
     const uint64_t budget = std::min<uint64_t>(32ull << 30, fr / 4);
     d.Vw = ((uint64_t)h->V * d.rs * 8ull <= budget) ? h->V : h->Vd;
+    if (h->branches == 2) d.Vw = 0;  // the two-branch mode does not use the three-branch records
   }
   EZ_ALLOC(h, d.wrow, double, (size_t)d.Vw * d.rs);
+  if (h->branches == 2 && !ezl::two_branch_word_major(h->K)) {
+    EZ_ALLOC(h, d.tbw, double, (size_t)h->V * d.Kpad);
+    EZ_ALLOC(h, d.tbq, double, (size_t)h->V * d.Kpad);
+  }
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
   EZ_ALLOC(h, d.ctr, ezl::Counters, 1);
@@ -898,6 +905,8 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   }
   if (o.g > 3) return bad(EZLDA_E_INVALID, "g must be in {1,2,3} (0 = default 2)");
   if (o.w_mode > 2) return bad(EZLDA_E_INVALID, "unknown w_mode");
+  if (o.sampler != 0 && o.sampler != 2 && o.sampler != 3)
+    return bad(EZLDA_E_INVALID, "sampler must be 0/3 (three-branch) or 2 (two-branch)");
   ezlda* h = new (std::nothrow) ezlda();
   if (!h) return bad(EZLDA_E_NOMEM, "host allocation failed");
   h->N = n_tokens;
@@ -912,6 +921,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   h->world = o.world > 1 ? o.world : 1;
   h->timing = !o.no_phase_timing;
   h->exact_all = o.exact_draws ? 1u : 0u;
+  h->branches = o.sampler ? o.sampler : 3u;
   h->dev.token_base = o.token_base;
   ezlda_status st = EZLDA_OK;
   if (o.stream) {
@@ -971,12 +981,22 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     EZ_CUDA(h, cudaMemsetAsync(nxt.nk, 0, sizeof(int32_t) * h->K, s));
     EZ_CUDA(h, cudaMemsetAsync(nxt.tnnz, 0, sizeof(uint32_t) * std::max<uint32_t>(h->Vt, 1), s));
     ezl::launch_den(h->dev, cur, s);
-    ezl::launch_word_prep(h->dev, cur, s);
-    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
-    ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);
-    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
-    ezl::launch_sampler(h->dev, cur, nxt, h->n_items, i, false, s);
-    if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
+    if (h->branches == 2) {
+      // two-branch (ESCA) mode: D rebuild without the skip test, What / Q tables, one draw
+      // per token, then W / n_k of the new topics from the item histograms
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
+      ezl::launch_doc_pass(h->dev, cur, cur, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, false, s);
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
+      ezl::launch_two_branch(h->dev, cur, nxt, h->n_items, i, s);
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
+    } else {
+      ezl::launch_word_prep(h->dev, cur, s);
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
+      ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
+      ezl::launch_sampler(h->dev, cur, nxt, h->n_items, i, false, s);
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
+    }
     EZ_CUDA(h, cudaGetLastError());
     ezlda_status st;
     if ((st = allreduce(h, nxt.Wd, (size_t)h->Vd * h->K, ncclInt32))) return st;
@@ -984,7 +1004,10 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaEventRecord(ev[4], s));
     sl.iteration = i;
+    // den, word-prep, doc pass tiers, sampler; two-branch: den, doc pass tiers, then one
+    // word-major kernel, or What/Q tables + doc-major draw + W count
     sl.launches = 3u + (h->n_docs_w ? 1u : 0u) + (h->n_docs_b ? 1u : 0u) - (h->n_items ? 0u : 1u);
+    if (h->branches == 2) sl.launches = ezl::two_branch_word_major(h->K) ? sl.launches - 1u : sl.launches + 1u;
     h->pending.push_back(si);
     h->cur = 1 - h->cur;
     h->iteration = i;

@@ -1563,6 +1563,147 @@ __global__ void k_sum(const double* partial, uint32_t n, double* out) {
 }
 
 // ---------------------------------------------------------------------------------
+// Two-branch (ESCA) sampler mode (NEXT-1 of SURVEY 8(f); Eq (3)-(4) P:344-402, Alg
+// P:1481-1507, reading #11 of SURVEY 8(c)): the paper's own baseline, with neither the MPT
+// skip test nor the K1 split; it runs on the same D rebuild (doc pass without the skip
+// test) and W rebuild (item histograms of the new topics).
+//   k_tb_prep  block per word: What row (Eq 1-2) and the Q tree prefix
+//              QP2(k) = sum_{j<=k} alpha What_j (ascending, fp64, thread 0) in HBM
+//   k_tb_draw  warp per doc, lane per token: S = ascending sum over the packed D row of
+//              D[d][k] What[v][k], Z = S + Q; the S tree if u <= S / Z with u' = u Z,
+//              else the Q tree with u' = (1 - u) Z (the Fig 2 text)
+// Every operation is the oracle's, in its order (build flag -fmad=false), so the topics
+// are bit-identical without a certification step.  Not tuned: it exists to compare.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_tb_prep(Dev d, Buf cur) {
+  const uint32_t v = blockIdx.x;
+  double* row = d.tbw + (size_t)v * d.Kpad;
+  stage_row(d, cur, v, row);  // ends with __syncthreads: the row is visible block-wide
+  if (threadIdx.x == 0) {
+    double* q = d.tbq + (size_t)v * d.Kpad;
+    double acc = 0.0;
+#pragma unroll 8
+    for (uint32_t k = 0; k < d.K; ++k) {
+      acc = acc + d.alpha * row[k];
+      q[k] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t doc = blockIdx.x * 8u + (threadIdx.x >> 5);
+  if (doc >= d.Dn) return;
+  const uint32_t base = __ldg(d.ddb + doc);
+  const uint32_t nnz = __ldg(d.D + base) & 0xFFFFu;
+  const uint32_t* E = d.D + base + kDHdr;
+  const uint32_t j0 = __ldg(d.dofs + doc), j1 = __ldg(d.dofs + doc + 1);
+  for (uint32_t j = j0 + lane; j < j1; j += 32u) {
+    const uint32_t v = __ldg(d.tw + j);
+    const double* wh = d.tbw + (size_t)v * d.Kpad;
+    const double* qp = d.tbq + (size_t)v * d.Kpad;
+    double S = 0.0;
+    for (uint32_t e = 0; e < nnz; ++e) {
+      const uint32_t w = __ldg(E + e);
+      S = S + (double)(w & 0xFFFFu) * __ldg(wh + d_topic(w));
+    }
+    const double Q = __ldg(qp + d.K - 1u);
+    const double Z = S + Q;
+    const double u = philox_u(d.seed, iter, d.token_base + j);
+    uint32_t topic = d.K - 1u;
+    if (u <= S / Z) {  // S tree: first topic of the row whose prefix exceeds u Z, else the last
+      const double up = u * Z;
+      double acc = 0.0;
+      for (uint32_t e = 0; e < nnz; ++e) {
+        const uint32_t w = __ldg(E + e);
+        const uint32_t k = d_topic(w);
+        acc = acc + (double)(w & 0xFFFFu) * __ldg(wh + k);
+        topic = k;
+        if (acc > up) break;
+      }
+    } else {  // Q tree: first k with QP2(k) > (1 - u) Z (QP2 is non-decreasing), else K - 1
+      const double up = (1.0 - u) * Z;
+      uint32_t a = 0, b = d.K - 1u;
+      while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if (__ldg(qp + mid) > up) b = mid; else a = mid + 1u;
+      }
+      topic = a;
+    }
+    nxt.z[j] = (uint16_t)topic;
+  }
+  if (lane == 0) atomicAdd(&d.ctr->sampled, (unsigned long long)(j1 - j0));
+}
+
+// Word-major form (the paper's ESCA layout, K <= kTbItemMaxK): block per work item (word,
+// run range): the word's What row and Q prefix in shared memory, thread per (doc, word) run
+// (S once per run from the packed D row, then the run's tokens), the new topics into the
+// item's histogram and W / n_k rebuilt from it in the same kernel (as the three-branch
+// sampler does).  Same operations and orders as k_tb_draw.
+__global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32_t iter) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* wh = reinterpret_cast<double*>(smem);
+  double* qp = wh + d.Kpad;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qp + d.Kpad);
+  __shared__ uint32_t s_wsum[32], s_run;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t item = blockIdx.x;
+  const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
+  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+  stage_row(d, cur, v, wh);  // ends with __syncthreads
+  if (tid == 0) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (uint32_t k = 0; k < d.K; ++k) {
+      acc = acc + d.alpha * wh[k];
+      qp[k] = acc;
+    }
+  }
+  __syncthreads();
+  const double Q = qp[d.K - 1u];
+  for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) {
+    const uint32_t j0 = __ldg(d.run_j0 + r), len = __ldg(d.run_len + r), base = __ldg(d.run_dbase + r);
+    const uint32_t nnz = __ldg(d.D + base) & 0xFFFFu;
+    const uint32_t* E = d.D + base + kDHdr;
+    double S = 0.0;
+    for (uint32_t e = 0; e < nnz; ++e) {
+      const uint32_t w = __ldg(E + e);
+      S = S + (double)(w & 0xFFFFu) * wh[d_topic(w)];
+    }
+    const double Z = S + Q;
+    for (uint32_t t = 0; t < len; ++t) {
+      const uint32_t j = j0 + t;
+      const double u = philox_u(d.seed, iter, d.token_base + j);
+      uint32_t topic = d.K - 1u;
+      if (u <= S / Z) {
+        const double up = u * Z;
+        double acc = 0.0;
+        for (uint32_t e = 0; e < nnz; ++e) {
+          const uint32_t w = __ldg(E + e);
+          const uint32_t k = d_topic(w);
+          acc = acc + (double)(w & 0xFFFFu) * wh[k];
+          topic = k;
+          if (acc > up) break;
+        }
+      } else {
+        const double up = (1.0 - u) * Z;
+        uint32_t a = 0, b = d.K - 1u;
+        while (a < b) {
+          const uint32_t mid = (a + b) >> 1;
+          if (qp[mid] > up) b = mid; else a = mid + 1u;
+        }
+        topic = a;
+      }
+      nxt.z[j] = (uint16_t)topic;
+      atomicAdd(&hist[topic], 1u);
+    }
+  }
+  __syncthreads();
+  item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
+  if (tid == 0) atomicAdd(&d.ctr->sampled, (unsigned long long)d.item_ntok[item]);
+}
+
+// ---------------------------------------------------------------------------------
 // setup / IO
 // ---------------------------------------------------------------------------------
 __global__ void k_init_topics(Dev d, uint16_t* z) {
@@ -1633,6 +1774,12 @@ SamplerLayout sampler_layout(uint32_t K) {
 uint32_t sampler_slots(uint32_t K) { return sampler_layout(K).nslots; }
 size_t sampler_smem_bytes(uint32_t K) { return sampler_layout(K).smem_bytes; }
 size_t wcount_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
+static size_t tb_item_smem_bytes(uint32_t K) {
+  const size_t Kpad = (K + 31) / 32 * 32;
+  return Kpad * 8 * 2 + Kpad * 4;
+}
+bool two_branch_word_major(uint32_t K) { return tb_item_smem_bytes(K) <= 200u * 1024u; }
+
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
@@ -1668,6 +1815,9 @@ cudaError_t configure_kernels(uint32_t K) {
     g_sampler_grid = (uint32_t)(nsm * nb);
   }
   if ((e = cudaFuncSetAttribute(k_wcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wcount_smem_bytes(K))))
+    return e;
+  if (two_branch_word_major(K) &&
+      (e = cudaFuncSetAttribute(k_tb_item, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_item_smem_bytes(K))))
     return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
   if ((e = cudaFuncSetAttribute(k_doc_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
@@ -1727,6 +1877,17 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
       void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
       cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);
     }
+}
+
+void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
+                       cudaStream_t s) {
+  if (two_branch_word_major(d.K)) {
+    if (n_items) k_tb_item<<<n_items, 256, tb_item_smem_bytes(d.K), s>>>(d, cur, nxt, iteration);
+    return;
+  }
+  k_tb_prep<<<d.V, 256, 0, s>>>(d, cur);
+  k_tb_draw<<<(d.Dn + 7) / 8, 256, 0, s>>>(d, nxt, iteration);
+  if (n_items) k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, nxt, nxt);
 }
 
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {

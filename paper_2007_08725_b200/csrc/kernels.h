@@ -60,6 +60,9 @@ struct Dev {
   uint32_t* hist_scratch;  // [grid * nslots * Kpad] (zero between items)
   double* qp_scratch;      // [grid * nslots * 1.5 Kpad] exact Q' (+ fixed-point) tables of warp-staged tail rows
   uint32_t exact_all;  // 1: every sampled token takes the exact fp64 path (test/ablation knob)
+  uint32_t branches;   // 3: three-branch sampler (default); 2: two-branch ESCA mode (NEXT-1)
+  double* tbw;         // two-branch mode: [V * Kpad] What rows (Eq 1-2)
+  double* tbq;         // two-branch mode: [V * Kpad] Q tree prefix sum_{j<=k} alpha What_j
   uint32_t Vw;     // words v < Vw have their What' | QP row precomputed in wrow (Vd, or V if it fits)
   uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, 0x7FFF)
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
@@ -108,6 +111,13 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
 // sampler over items; count_only=true rebuilds W/n_k of `cur.z` into `nxt` (init, set_topics)
 void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
                     bool count_only, cudaStream_t s);
+// two-branch (ESCA) mode: What rows + Q prefixes of every word, then one draw per token
+// (D rows already rebuilt from cur.z) into nxt.z
+// (and W / n_k of the new topics into nxt).  K small enough for the word's tables in shared
+// memory: one word-major kernel; else What / Q tables in HBM, a doc-major draw, k_wcount.
+void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
+                       cudaStream_t s);
+bool two_branch_word_major(uint32_t K);
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s);
 
 // ----- setup / IO kernels -----

@@ -28,7 +28,7 @@ class Options(C.Structure):
         ("split_threshold", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32),
         ("nccl_unique_id", C.c_void_p), ("token_base", C.c_uint64), ("stream", C.c_void_p),
         ("input_on_device", C.c_uint32), ("no_phase_timing", C.c_uint32), ("doc_block_kb", C.c_uint32),
-        ("exact_draws", C.c_uint32), ("pad0", C.c_uint32), ("local_group", C.c_uint64),
+        ("exact_draws", C.c_uint32), ("sampler", C.c_uint32), ("local_group", C.c_uint64),
     ]
 
 
@@ -115,7 +115,7 @@ class EzLDA:
                  dense_threshold: int = 0, split_threshold: int = 0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, token_base: int = 0, stream: int | None = None,
                  phase_timing: bool = True, doc_block_kb: int = 0, exact_draws: bool = False,
-                 local_group: int = 0):
+                 local_group: int = 0, sampler: int = 3):
         L = load()
         self._h = None
         on_dev = bool(getattr(word_ids, "is_cuda", False))
@@ -139,6 +139,7 @@ class EzLDA:
         o.doc_block_kb = doc_block_kb
         o.exact_draws = 1 if exact_draws else 0
         o.local_group = local_group
+        o.sampler = sampler  # 3: three-branch (default), 2: two-branch ESCA baseline mode
         h = C.c_void_p()
         rc = L.ezlda_create(_addr(word_ids), _addr(doc_ids), self.N, self.n_docs, self.V, self.K, self.alpha,
                             self.beta, seed, C.byref(o), C.byref(h))

@@ -332,3 +332,41 @@ def test_multi_rank_library_path_one_gpu(ez, world):
         assert np.array_equal(out[r][1], W_ref), r
         assert np.array_equal(out[r][2], nk_ref), r
         assert abs(out[r][3] - ll_ref) <= 1e-12 * abs(ll_ref), (out[r][3], ll_ref)
+
+
+TWO_BRANCH_CASES = {
+    "tiny_K16": (dict(n_docs=100, V=500, mean_len=100.0, sigma=0.5), 16, 12),
+    "small_K64": (dict(n_docs=2000, V=5000, mean_len=90.0, sigma=0.5), 64, 4),
+    "long_docs_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 2),
+    "K5000": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 5000, 2),
+    # K too large for the word's tables in shared memory: HBM tables + doc-major draw + W count
+    "K16384_hbm_tables": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 16384, 2),
+}
+
+
+@pytest.mark.parametrize("case", list(TWO_BRANCH_CASES))
+def test_two_branch_mode_parity(ez, oracle_mod, case):
+    """sampler=2 (two-branch ESCA mode, NEXT-1, reading #11): one-step parity with
+    the oracle's two-branch chain, bit-identical topics, exact D / W / n_k, no skipping."""
+    spec, K, iters = TWO_BRANCH_CASES[case]
+    w, d = planted_corpus_np(**spec)
+    n_docs, V = spec["n_docs"], spec["V"]
+    gpu = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, sampler=2)
+    orc = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, branches=2)
+    chain = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, branches=2)
+    z = gpu.topics()
+    assert np.array_equal(z, orc.topics())
+    for i in range(1, iters + 1):
+        orc.set_topics(z, i - 1)
+        orc.iterate(1)
+        chain.iterate(1)
+        gpu.iterate(1)
+        zg = gpu.topics()
+        assert np.array_equal(zg, orc.topics()), (i, int((zg != orc.topics()).sum()))
+        st = gpu.stats()
+        assert st["skip_S"] == 0 and st["sampled"] == len(zg)
+        check_counts(ez, gpu, w, d, n_docs, V, K, zg)
+        z = zg
+    # chain parity: the independent oracle chain reached the same state
+    assert np.array_equal(gpu.topics(), chain.topics())
+    assert abs(gpu.loglik() - chain.loglik(1)) <= 1e-10 * abs(chain.loglik(1))
