@@ -328,47 +328,73 @@ __device__ __forceinline__ void what_reset(const Dev& d, const Buf& cur, uint32_
   }
 }
 
+constexpr uint32_t kWpChunk = 16;  // k_word_prep_t: entries per lane between cooperative row writes
+
 __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31u;
+  // pass-2 outputs of the warp's 32 words, staged per 16-entry chunk so that every row is
+  // written with contiguous stores instead of 32 scattered rows per store instruction
+  __shared__ uint32_t s_m[4][32][kWpChunk + 1];
+  __shared__ double s_q[4][32][kWpChunk + 1];
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31u, wi = threadIdx.x >> 5;
   const bool act = v < d.V && d.wtok[v + 1] != d.wtok[v];  // else no token of v in this shard
   const bool out = act && v < d.Vw;
+  const uint32_t outmask = __ballot_sync(kFull, out);
+  const uint32_t vbase = v - lane;
   double two_t = 0.0;
+  WhatCursor c;
+  WordRec r;
+  uint32_t K1 = 0xFFFFFFFFu;
+  int sh = 0;
   if (act) {
-    WhatCursor c;
     what_reset(d, cur, v, c);
     Top4 t;
     top4_init(t);
     for (uint32_t k = 0; k < d.K; ++k) top4_insert(t, what_next(d, c, k), k);
-    WordRec r;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const bool ok = t.v[i] >= 0.0;
       r.a[i] = ok ? t.v[i] : 0.0;
       r.K[i] = ok ? (uint16_t)t.k[i] : (uint16_t)0;
     }
-    const uint32_t K1 = r.K[0];
-    WrowPtrs o = wrow_ptrs(d, v);
+    K1 = r.K[0];
     int e = 0;
     frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
-    const int sh = 32 - e;
+    sh = 32 - e;
     if (out) {
+      WrowPtrs o = wrow_ptrs(d, v);
       o.sc[0] = ldexp(1.0, -sh);
       o.sc[1] = ldexp(1.0, sh);
     }
     what_reset(d, cur, v, c);
-    double acc = 0.0;
-    for (uint32_t k = 0; k < d.Kpad; ++k) {
-      double w = (k < d.K) ? what_next(d, c, k) : 0.0;
+  }
+  double acc = 0.0;
+  for (uint32_t k0 = 0; k0 < d.Kpad; k0 += kWpChunk) {  // warp-uniform trip count (Kpad % 32 == 0)
+#pragma unroll 4
+    for (uint32_t i = 0; i < kWpChunk; ++i) {
+      const uint32_t k = k0 + i;
+      double w = (act && k < d.K) ? what_next(d, c, k) : 0.0;
       if (k == K1) w = 0.0;  // What' (Eq 6): the maximum entry set to 0
       acc = acc + w;
       if (k == d.K - 1u) r.Qp = d.alpha * acc;
-      if (out) {
-        o.m[k] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
-        o.qp[k] = d.alpha * acc;
+      s_m[wi][lane][i] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
+      s_q[wi][lane][i] = d.alpha * acc;
+    }
+    __syncwarp();
+    for (uint32_t x = lane; x < 32u * kWpChunk; x += 32u) {
+      const uint32_t src = x / kWpChunk, kk = x % kWpChunk;
+      if ((outmask >> src) & 1u) {
+        WrowPtrs o = wrow_ptrs(d, vbase + src);
+        o.m[k0 + kk] = s_m[wi][src][kk];
+        o.qp[k0 + kk] = s_q[wi][src][kk];
       }
     }
+    __syncwarp();
+  }
+  if (act) {
     d.rec[v] = r;
     if (out) {
+      WrowPtrs o = wrow_ptrs(d, v);
+      int e = 0;
       frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
       two_t = ldexp(1.0, 32 - e);
       o.sc[2] = ldexp(1.0, e - 32);

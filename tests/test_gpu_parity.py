@@ -290,8 +290,9 @@ def test_invalid_arguments(ez):
         ez.EzLDA(long_doc, long_doc, 1, 1, 4)
 
 
+@pytest.mark.parametrize("sampler", [3, 2])
 @pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_library_path_one_gpu(ez, world):
+def test_multi_rank_library_path_one_gpu(ez, world, sampler):
     """The library's multi-rank path (doc shards with token bases, global word counts and
     relabelling, all-dense W merged every iteration, LLPT reduction) with the ranks as
     handles of this process on one GPU (options.local_group: the merge is an in-process
@@ -301,7 +302,7 @@ def test_multi_rank_library_path_one_gpu(ez, world):
 
     w, d = planted_corpus_np(n_docs=600, V=4000, mean_len=90.0, sigma=0.5, seed=17)
     n_docs, V, K, iters = 600, 4000, 64, 5
-    ref = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED)
+    ref = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, sampler=sampler)
     ref.iterate(iters)
     z_ref, nk_ref, ll_ref = ref.topics(), ref.n_k(), ref.loglik()
     W_ref = ez.EzLDA.csr_to_dense(*ref.W_csr(), K)
@@ -314,7 +315,7 @@ def test_multi_rank_library_path_one_gpu(ez, world):
         try:
             t0, t1 = int(cum[b[r]]), int(cum[b[r + 1]])
             h = ez.EzLDA(w[t0:t1], d[t0:t1] - b[r], b[r + 1] - b[r], V, K, seed=SAMPLER_SEED, rank=r, world=world,
-                         token_base=t0, local_group=1000 + world)
+                         token_base=t0, local_group=1000 + 10 * sampler + world, sampler=sampler)
             h.iterate(iters)
             out[r] = (h.topics(), ez.EzLDA.csr_to_dense(*h.W_csr(), K), h.n_k(), h.loglik())
         except Exception as e:  # surfaced below (the other ranks would wait forever otherwise)
@@ -370,3 +371,23 @@ def test_two_branch_mode_parity(ez, oracle_mod, case):
     # chain parity: the independent oracle chain reached the same state
     assert np.array_equal(gpu.topics(), chain.topics())
     assert abs(gpu.loglik() - chain.loglik(1)) <= 1e-10 * abs(chain.loglik(1))
+
+
+@pytest.mark.parametrize("sampler", [3, 2])
+def test_checkpoint_resume_is_exact(ez, small, sampler):
+    """Checkpoint = (topics, iterations done) from ezlda_counts; resume = a fresh handle +
+    ezlda_set_topics: the resumed chain equals the uninterrupted one bit for bit (the draws
+    are keyed by (token, iteration))."""
+    w, d = small
+    K = 64
+    a = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], K, seed=SAMPLER_SEED, sampler=sampler)
+    a.iterate(4)
+    ckpt = a.topics().copy()
+    a.iterate(4)
+    b = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], K, seed=SAMPLER_SEED, sampler=sampler)
+    b.set_topics(ckpt, 4)
+    b.iterate(4)
+    assert b.stats()["iteration"] == 8
+    assert np.array_equal(a.topics(), b.topics())
+    assert np.array_equal(a.n_k(), b.n_k())
+    assert a.loglik() == b.loglik()
