@@ -410,7 +410,19 @@ __global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
     const uint32_t vw = __shfl_sync(kFull, v, src);
     const double tt = __shfl_sync(kFull, two_t, src);
     WrowPtrs o = wrow_ptrs(d, vw);
-    for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(o.qp[k] * tt, 4294967295.0));
+    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane (qp and qfx
+      double x[8];                                      // share the buffer: no implicit reordering)
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t k = k0 + 32u * i + lane;
+        x[i] = (k < d.Kpad) ? o.qp[k] : 0.0;
+      }
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t k = k0 + 32u * i + lane;
+        if (k < d.Kpad) o.qfx[k] = __double2uint_rn(fmin(x[i] * tt, 4294967295.0));
+      }
+    }
     for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)
       o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(o.qp[32u * c + 31u] * tt, 4294967295.0)) : 0xFFFFFFFFu;
   }
