@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
 // m_v (Eq 6, K1 entry 0), the fixed-point Q' prefix table and their scales are staged in a
 // shared-memory slot with ONE TMA bulk copy (cp.async.bulk + mbarrier) of the word's wrow
 // head (tail rows word-prep did not precompute are staged by a warp).  Persistent blocks
-// own two slots and pipeline items through them (k_sampler below).  Warps take groups of
+// own 2-3 slots and pipeline items through them (k_sampler below).  Warps take groups of
 // 32 runs from the item's cursor, queue the flagged ones (a token of the run failed the doc
 // pass's MPT test) and process them in batches (P:546 steps 4-6):
 //
@@ -1142,7 +1142,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
 // while another warp finishes the previous item.
 // ---------------------------------------------------------------------------------
 #ifndef EZLDA_SLOTS
-#define EZLDA_SLOTS 2
+#define EZLDA_SLOTS 3
 #endif
 constexpr uint32_t kMaxSlots = EZLDA_SLOTS;  // slots per block when they fit (d.nslots: 1 for large K)
 constexpr uint32_t kExit = 0x80000000u;
@@ -1779,20 +1779,22 @@ uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= E
 }
 constexpr size_t kMaxSmem = 227u * 1024u;
 // shared-memory layout of the sampler block: kMaxSlots SlotCtl | nslots x (slot head [+ hist])
-// | kSampWarpsP x warp scratch.  Two slots with the histograms in shared memory when they fit,
-// else two slots with the histograms in HBM scratch, else one slot.
+// | kSampWarpsP x warp scratch.  kMaxSlots (3) slots with the histograms and the Q' table in
+// shared memory when they fit, else with the histograms / Q' table in HBM, else fewer slots.
 SamplerLayout sampler_layout(uint32_t K) {
   SamplerLayout L{};
   const uint32_t Kpad = (K + 31) / 32 * 32;
   L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it)
-  // with two slots; per budget: histograms and the Q' table in shared memory, else the
-  // histograms in HBM scratch, else also the Q' table in HBM; last resort one slot
+  // with >= 2 slots, the most slots first (A/B: 3 slots vs 2 -- PubMed 77.1 -> 76.0 ms,
+  // NYTimes K=5k 60.0 -> 46.0 ms; 4 slots slower); per slot count: histograms and the Q'
+  // table in shared memory, else the histograms in HBM scratch, else also the Q' table in
+  // HBM; last resort one block per SM
   const size_t budgets[2] = {(228u * 1024u) / EZLDA_SAMP_MINB - 1024u, kMaxSmem};
   for (size_t budget : budgets)
     for (uint32_t n = kMaxSlots; n >= 1; --n) {
-      if (n < kMaxSlots && budget != kMaxSmem) break;
+      if (n < 2u && budget != kMaxSmem) break;  // keep >= 2 slots when blocks share the SM
       for (uint32_t mode = 0; mode < 3; ++mode) {
         const uint32_t qg = mode == 2 ? 1u : 0u, hg = mode >= 1 ? 1u : 0u;
         const uint32_t head = slot_head_bytes(Kpad, qg);

@@ -17,3 +17,9 @@ bash tools/gpu_prof.sh pubmed ${tag} k_sampler 3
 bash tools/gpu_prof.sh pubmed ${tag}doc k_doc_hist 3
 timeout 600 python tools/curve.py --config pubmed --iters 200 --llpt-every 20 --csv gpurun_out/curve_pubmed_${tag}.csv 2>&1 | tail -1
 timeout 600 python tools/curve.py --config nytimes --iters 200 --llpt-every 20 --csv gpurun_out/curve_nytimes_${tag}.csv 2>&1 | tail -1
+for c in nytimes_k5k nytimes_k10k; do
+  timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline --no-e2e > gpurun_out/bench_${c}_${tag}.json 2>/dev/null; tail -c 120 gpurun_out/bench_${c}_${tag}.json
+done
+for c in pubmed nytimes; do
+  timeout 600 python bench.py --config $c --sampler 2 --steps 10 --no-cpu-baseline --no-e2e > gpurun_out/bench_two_branch_${c}_${tag}.json 2>/dev/null; tail -c 120 gpurun_out/bench_two_branch_${c}_${tag}.json
+done

@@ -26,3 +26,6 @@ for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
     print(f"{len(v):3d} launches {sum(v) / 1e6:9.2f} ms total {sum(v) / len(v) / 1e6:8.3f} ms/launch  iteration share {share}  {k}")
 PY
 grep -h "dram__bytes\|Duration" profiles/r01_ncu_sampler_pubmed_$T.txt profiles/r01_ncu_docpass_pubmed_$T.txt
+for f in gpurun_out/bench_nytimes_k5k_$T.json gpurun_out/bench_nytimes_k10k_$T.json gpurun_out/bench_two_branch_pubmed_$T.json gpurun_out/bench_two_branch_nytimes_$T.json; do
+  [ -f $f ] && cp $f profiles/r01_$(basename $f .json | sed "s/_$T\$//")_$T.json
+done
