@@ -124,7 +124,7 @@ class EzLDA:
             doc_ids = np.ascontiguousarray(doc_ids, dtype=np.uint32)
         self.N = int(word_ids.shape[0])
         self.n_docs, self.V, self.K = int(n_docs), int(V), int(K)
-        self.alpha = 50.0 / K if alpha is None else float(alpha)
+        self.alpha = (50.0 / K if K else 0.0) if alpha is None else float(alpha)  # K = 0: E_INVALID
         self.beta = float(beta)
         o = Options()
         o.struct_size = C.sizeof(Options)

@@ -73,3 +73,28 @@ def test_product_package_does_not_import_oracle():
                 code = re.sub(r"(#|//).*", "", txt)
                 code = re.sub(r'""".*?"""', "", code, flags=re.S)
                 assert "import oracle" not in code and "from oracle" not in code and "ezlda_oracle" not in code, fn
+
+
+@pytest.mark.parametrize("kw, status", [
+    (dict(K=0), "E_INVALID"),
+    (dict(alpha=-1.0), "E_INVALID"),
+    (dict(beta=0.0), "E_INVALID"),
+    (dict(g=4), "E_INVALID"),
+    (dict(w_mode=3), "E_INVALID"),
+    (dict(sampler=1), "E_INVALID"),
+    (dict(sampler=4), "E_INVALID"),
+    (dict(K=70000), "E_RANGE"),
+    (dict(K=16385), "E_RANGE"),
+])
+def test_create_validates_before_touching_the_device(lib_path, kw, status):
+    """ezlda_create rejects bad arguments with a status code (no exception or abort crosses
+    the ABI) before any CUDA call, so these run on a machine without a GPU."""
+    from paper_2007_08725_b200 import lda
+
+    args = dict(K=16)
+    args.update(kw)
+    K = args.pop("K")
+    w = [0, 1, 2]
+    d = [0, 0, 1]
+    with pytest.raises(lda.EzLDAError, match=status):
+        lda.EzLDA(w, d, 2, 3, K, **args)
