@@ -69,7 +69,10 @@ typedef struct {
   uint32_t dense_threshold;  /* HYBRID: dense iff c_v > this; 0 -> K              */
   uint32_t split_threshold;  /* large-word region size in tokens; 0 -> 10000     */
   int32_t rank;              /* this process's rank (doc shard index)                     */
-  int32_t world;             /* number of ranks; 0 or 1 = single GPU                       */
+  int32_t world;             /* number of ranks; 0 or 1 = single GPU.  world == 1 WITH      */
+                             /* nccl_unique_id set: a one-rank NCCL group running the       */
+                             /* multi-rank path (all-dense W, per-iteration ncclAllReduce)  */
+                             /* on one GPU -- exercises the NCCL calls (tests)              */
   const void* nccl_unique_id;/* 128-byte ncclUniqueId from rank 0 (caller broadcasts it)   */
   uint64_t token_base;       /* global doc-major index of this shard's first token (RNG)  */
   void* stream;              /* cudaStream_t to run on, or NULL (library creates one)      */

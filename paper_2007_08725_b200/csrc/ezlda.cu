@@ -208,6 +208,7 @@ inline unsigned blocks(uint64_t n, unsigned t = 256) { return (unsigned)((n + t 
 // ----------------------------------------------------------------------------
 struct ezlda {
   void* lgroup = nullptr;  // LocalGroup* of the in-process rank group (options.local_group), else NCCL
+  bool multi = false;      // multi-rank path: world > 1, or a one-rank NCCL group (world == 1 + nccl id)
   Dev dev{};
   Buf buf[2]{};
   int cur = 0;
@@ -395,7 +396,7 @@ ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t d
 }
 
 ezlda_status allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
-  if (h->world <= 1 || count == 0) return EZLDA_OK;
+  if (!h->multi || count == 0) return EZLDA_OK;
   if (h->lgroup) return local_allreduce(h, buf, count, dt);
   EZ_NCCL(h, nccl().AllReduce(buf, buf, count, dt, ncclSum, h->comm, h->stream));
   return EZLDA_OK;
@@ -506,7 +507,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   // global word counts (the dense/tail split and relabelling must agree on all ranks)
   std::vector<uint64_t> cnt(h->V);
   for (uint32_t v = 0; v < h->V; ++v) cnt[v] = cnt_local[v];
-  if (h->world > 1) {
+  if (h->multi) {
     uint64_t* d_c64;
     EZ_ALLOC(h, d_c64, uint64_t, h->V);
     EZ_CUDA(h, cudaMemcpyAsync(d_c64, cnt.data(), sizeof(uint64_t) * h->V, cudaMemcpyHostToDevice, s));
@@ -540,7 +541,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   uint32_t Vd = 0;
   while (Vd < h->V && (cnt[h->origword[Vd]] > thr || cnt[h->origword[Vd]] > 65535)) ++Vd;
   // world > 1: W is merged by an int32 all-reduce of dense rows (tail all-gather: next round)
-  if (o.w_mode == EZLDA_W_ALL_DENSE || h->world > 1) Vd = h->V;
+  if (o.w_mode == EZLDA_W_ALL_DENSE || h->multi) Vd = h->V;
   h->Vd = Vd;
   h->Vt = h->V - Vd;
   std::vector<uint32_t> tofs(h->Vt + 1, 0);
@@ -919,6 +920,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   h->g = o.g ? o.g : 2;
   h->rank = o.rank;
   h->world = o.world > 1 ? o.world : 1;
+  h->multi = o.world > 1 || (o.world == 1 && o.nccl_unique_id != nullptr);
   h->timing = !o.no_phase_timing;
   h->exact_all = o.exact_draws ? 1u : 0u;
   h->branches = o.sampler ? o.sampler : 3u;
@@ -934,12 +936,12 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
     }
     h->own_stream = true;
   }
-  if (h->world > 1 && o.local_group) {
+  if (h->multi && o.local_group) {
     if (o.rank < 0 || o.rank >= h->world) st = h->fail(EZLDA_E_INVALID, "local_group needs 0 <= rank < world");
     else h->lgroup = local_group(o.local_group, h->world);
-  } else if (h->world > 1) {
+  } else if (h->multi) {
     if (!o.nccl_unique_id || o.rank < 0 || o.rank >= h->world) {
-      st = h->fail(EZLDA_E_INVALID, "world > 1 needs nccl_unique_id and 0 <= rank < world");
+      st = h->fail(EZLDA_E_INVALID, "world >= 1 with NCCL needs nccl_unique_id and 0 <= rank < world");
     } else if (!nccl().ok) {
       st = h->fail(EZLDA_E_NCCL, "libnccl.so.2 could not be loaded");
     } else {

@@ -391,3 +391,22 @@ def test_checkpoint_resume_is_exact(ez, small, sampler):
     assert np.array_equal(a.topics(), b.topics())
     assert np.array_equal(a.n_k(), b.n_k())
     assert a.loglik() == b.loglik()
+
+
+@pytest.mark.parametrize("sampler", [3, 2])
+def test_one_rank_nccl_group_matches_single_gpu(ez, sampler):
+    """world = 1 with an ncclUniqueId: the library's multi-rank path -- global word counts
+    all-reduced at create, every W row dense, W and n_k merged by ncclAllReduce every
+    iteration, LLPT reduced -- through a real one-rank NCCL communicator (the only NCCL
+    group one GPU can hold).  Topics, W, n_k and LLPT equal the single-GPU chain bit for bit."""
+    w, d = planted_corpus_np(n_docs=600, V=4000, mean_len=90.0, sigma=0.5, seed=17)
+    n_docs, V, K, iters = 600, 4000, 64, 5
+    ref = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, sampler=sampler)
+    ref.iterate(iters)
+    h = ez.EzLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, sampler=sampler, rank=0, world=1,
+                 nccl_id=ez.nccl_unique_id())
+    h.iterate(iters)
+    assert np.array_equal(h.topics(), ref.topics())
+    assert np.array_equal(ez.EzLDA.csr_to_dense(*h.W_csr(), K), ez.EzLDA.csr_to_dense(*ref.W_csr(), K))
+    assert np.array_equal(h.n_k(), ref.n_k())
+    assert h.loglik() == ref.loglik()
