@@ -495,8 +495,11 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
 // 32-topic words: popcount prefix + set-bit walk, O(nnz + K/32) per doc) and both are
 // re-zeroed as they are read.
 template <bool kSkipTest>
+#ifndef EZLDA_DOC_PF
+#define EZLDA_DOC_PF 1
+#endif
 #ifndef EZLDA_DOC_MINB
-#define EZLDA_DOC_MINB 1
+#define EZLDA_DOC_MINB 4
 #endif
 __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev d, Buf cur, Buf nxt, const uint32_t* docs,
                                                               uint32_t n_docs, uint32_t iter) {
@@ -509,10 +512,34 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
   for (uint32_t i = lane; i < hw + bw; i += 32) hist[i] = 0;
   __syncwarp();
   unsigned long long n_skip = 0, n_nnz = 0;
+#if EZLDA_DOC_PF
+  // the next doc's id, token range and D-row base are loaded one doc ahead (the chain
+  // docs -> dofs -> tokens otherwise starts every doc with two dependent global loads)
+  const uint32_t stride = gridDim.x * kDocWarps;
+  uint32_t idx = blockIdx.x * kDocWarps + warp;
+  uint32_t n_doc = 0, n_j0 = 0, n_j1 = 0, n_db = 0;
+  if (idx < n_docs) {
+    n_doc = docs[idx];
+    n_j0 = d.dofs[n_doc];
+    n_j1 = d.dofs[n_doc + 1];
+    n_db = d.ddb[n_doc];
+  }
+  for (; idx < n_docs; idx += stride) {
+    const uint32_t doc = n_doc, j0 = n_j0, L = n_j1 - n_j0, dbase = n_db;
+    (void)doc;
+    if (idx + stride < n_docs) {
+      n_doc = docs[idx + stride];
+      n_j0 = d.dofs[n_doc];
+      n_j1 = d.dofs[n_doc + 1];
+      n_db = d.ddb[n_doc];
+    }
+#else
   for (uint32_t idx = blockIdx.x * kDocWarps + warp; idx < n_docs; idx += gridDim.x * kDocWarps) {
     const uint32_t doc = docs[idx];
     const uint32_t j0 = d.dofs[doc];
     const uint32_t L = d.dofs[doc + 1] - j0;
+    const uint32_t dbase = d.ddb[doc];
+#endif
     // the first kPre tokens of each lane: topic, word and run id loaded together (the
     // skip test's word records then depend on one load round instead of two)
     constexpr uint32_t kPre = 4;
@@ -547,7 +574,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
         mpt_token(d, nxt, j0 + i, L, iter, d.tw[j0 + i], d.trid[j0 + i], C, n_skip);
       __syncwarp();
     }
-    uint32_t* Drow = d.D + d.ddb[doc] + kDHdr;
+    uint32_t* Drow = d.D + dbase + kDHdr;
     uint32_t nnz = 0;
     for (uint32_t base = 0; base < bw; base += 32) {
       const uint32_t wi = base + lane;
