@@ -651,7 +651,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   const uint32_t blk_words = (uint32_t)std::min<uint64_t>(blk_kb * 256ull, 0xFFFFFFFFull);
   const uint64_t nwin = (h->Dwords + blk_words - 1) / blk_words;
 #ifndef EZLDA_WIN_TOK
-#define EZLDA_WIN_TOK 1024  // window-cut only words with >= 1024 tokens per D window on average (A/B: 256 .. 16384)
+#define EZLDA_WIN_TOK 512  // window-cut only words with >= 512 tokens per D window on average (A/B: 256 .. 16384)
 #endif
   const uint32_t cut_min = (uint32_t)std::min<uint64_t>((uint64_t)EZLDA_WIN_TOK * nwin, 0xFFFFFFFFull);
   h->cut_min = cut_min;

@@ -24,7 +24,10 @@ namespace ezl {
 namespace {
 
 constexpr int kDocWarpCap = 512; // doc-pass warp tier: documents up to 512 tokens
-constexpr int kDocWarps = 8;
+#ifndef EZLDA_DOC_WARPS
+#define EZLDA_DOC_WARPS 8
+#endif
+constexpr int kDocWarps = EZLDA_DOC_WARPS;
 constexpr int kLlptWarps = 8;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
