@@ -19,8 +19,11 @@
  *     iteration 0 draws z^0 = floor(r0 K / 2^32);
  *   - interval layout [M | S' | Q'] with ascending-topic prefixes, ties to the
  *     smaller topic, and S_est of Eq (10) with depth g.
- * Results do not depend on the performance knobs (dense threshold, split
- * threshold, g, number of GPUs) beyond fp64 rounding at bucket boundaries.
+ * The topics are bit-identical to the CPU oracle's (oracle/, test infrastructure)
+ * and do not depend on the performance knobs (dense threshold, split threshold, g,
+ * W storage mode, number of GPUs, exact_draws).  options.sampler = 2 selects the
+ * paper's two-branch (ESCA) map instead (Eq 3-4): the same conditional,
+ * a different chain, equal to the oracle's two-branch chain bit for bit.
  *
  * Conventions
  *   - Ownership: input arrays are read during the call only and copied; output
