@@ -30,7 +30,7 @@ def free_port():
     return p
 
 
-def worker(rank, world, port, out):
+def worker(rank, world, port, out, branches=3):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,7 +42,7 @@ def worker(rank, world, port, out):
     cum = np.concatenate([[0], np.cumsum(L)])
     t0, t1 = int(cum[bounds[rank]]), int(cum[bounds[rank + 1]])
     shard = oracle.OracleLDA(w[t0:t1], d[t0:t1] - bounds[rank], bounds[rank + 1] - bounds[rank], V, K,
-                             seed=SAMPLER_SEED, token_base=t0)
+                             seed=SAMPLER_SEED, token_base=t0, branches=branches)
     for _ in range(ITERS):
         Wl = torch.from_numpy(shard.counts()[1].astype(np.int64))
         dist.all_reduce(Wl, op=dist.ReduceOp.SUM)  # the per-iteration W merge
@@ -71,13 +71,16 @@ def test_partition_docs_balanced():
         assert max(tok) - min(tok) <= 2 * L.max()
 
 
-def test_two_rank_gloo_equals_single(tmp_path):
+@pytest.mark.parametrize("branches", [3, 2])
+def test_two_rank_gloo_equals_single(tmp_path, branches):
+    """Doc shards + a summed W every iteration reproduce the single chain bit for bit, for the
+    three-branch sampler and the two-branch (ESCA) mode alike."""
     from oracle import oracle
 
     oracle.build()
     out = str(tmp_path / "z.npy")
-    mp.spawn(worker, args=(2, free_port(), out), nprocs=2, join=True)
+    mp.spawn(worker, args=(2, free_port(), out, branches), nprocs=2, join=True)
     w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
-    ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED)
+    ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED, branches=branches)
     ref.iterate(ITERS)
     assert np.array_equal(np.load(out), ref.topics().astype(np.int64))
