@@ -17,7 +17,9 @@
  * Random123 Philox4x32-10 known-answer vectors, brute-force u-measure of each
  * topic vs the textbook conditional Eq (1)/(2), S_est >= S',
  * topic invariance across g, count invariants, K=1 unigram LLPT
- * closed form (Eq 5), dense-vs-identity LLPT cross-check.
+ * closed form (Eq 5), dense-vs-identity LLPT cross-check; the two-branch
+ * (ESCA) draw and chain (ezlda_oracle_set_sampler): u-measure of every topic equals the
+ * textbook conditional, count invariants, LLPT rise, doc-shard emulation.
  * Parity pinned for every exported function except as stated in DESIGN.md.
  */
 #ifndef EZLDA_ORACLE_H
