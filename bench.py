@@ -125,7 +125,20 @@ def time_oracle(cfg, target_tokens: int, iters: int, warmup: int = 0):
     return len(w) * iters / dt, len(w), n_docs, dt
 
 
-def run_reference(args, rank):
+def arm_config(cfg, args, world: int) -> dict:
+    """The workload both arms report (ours and --impl reference print the same dict)."""
+    return {"workload": f"{cfg.name}-shaped synthetic LDA", "docs": cfg.n_docs, "V": cfg.V, "K": cfg.K,
+            "mean_doc_len": cfg.mean_len, "doc_len_sigma": cfg.sigma, "alpha": cfg.alpha, "beta": cfg.beta,
+            "g": args.g, "w_mode": args.w_mode, "split_threshold": args.split or 10000,
+            "exact_draws": bool(args.exact_draws),
+            "sampler": "two-branch (ESCA)" if args.sampler == 2 else "three-branch",
+            "iterations_timed": [args.warmup + 1, args.warmup + args.steps],
+            "parallelism": f"doc-partitioned x{world}",
+            "l2": "inputs exceed L2 (corpus state "
+                  f">{(int(cfg.n_docs * cfg.mean_len) * 12) >> 30} GiB vs 126 MB L2); no flush"}
+
+
+def run_reference(args, rank, world=1):
     """--impl reference: the CPU oracle as it stands, on the host cores, on a bounded sample."""
     if rank != 0:
         return 0
@@ -135,8 +148,7 @@ def run_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}-shaped sample", "K": cfg.K, "V": cfg.V, "sample_tokens": n,
-                   "sample_docs": n_docs},
+        "config": arm_config(cfg, args, world),
         "cpu_baseline": {"value": tps, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"{n} tokens / {n_docs} docs of the {cfg.name}-shaped recipe (V={cfg.V}, "
                                    f"K={cfg.K}), iterations {args.warmup + 1}..{args.warmup + args.steps}, "
@@ -174,7 +186,7 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
-        return run_reference(args, rank)
+        return run_reference(args, rank, world)
 
     import torch
     import torch.distributed as dist
@@ -283,15 +295,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}-shaped synthetic LDA", "docs": cfg.n_docs, "V": cfg.V, "K": cfg.K,
-                   "tokens": N_global, "mean_doc_len": cfg.mean_len, "doc_len_sigma": cfg.sigma,
-                   "alpha": cfg.alpha, "beta": cfg.beta, "g": args.g, "w_mode": args.w_mode,
-                   "split_threshold": args.split or 10000, "exact_draws": bool(args.exact_draws),
-                   "sampler": "two-branch (ESCA)" if args.sampler == 2 else "three-branch",
-                   "iterations_timed": [args.warmup + 1,
-                                                                                     args.warmup + args.steps],
-                   "parallelism": f"doc-partitioned x{world}", "l2": "inputs exceed L2 (corpus state "
-                   f">{(N_global * 12) >> 30} GiB vs 126 MB L2); no flush"},
+        "config": arm_config(cfg, args, world),
+        "tokens_per_step": N_global,
         "roofline": roof,
         "gpu_launches": int(S["kernel_launches"]),
         "phases_ms_per_step": {"wordprep": S["ms_wordprep"] / args.steps, "docpass": S["ms_docpass"] / args.steps,
