@@ -35,7 +35,7 @@
  *     and the stream given in the options (or one it creates).
  *   - Threading: one handle per host thread; calls on a handle are serialised.
  *   - Limits (16+16-bit packing): K <= 65535, doc length <= 65535,
- *     tokens per shard < 2^32.  This build additionally requires K <= 16384 (the
+ *     tokens per shard < 2^31 (the setup sorts index tokens with int).  This build additionally requires K <= 16384 (the
  *     packed D entries hold the topic in 14 bits; NEXT-2 lifts it).
  */
 #ifndef EZLDA_H
@@ -53,7 +53,7 @@ typedef struct ezlda ezlda; /* opaque; owned by the library */
 typedef enum {
   EZLDA_OK = 0,
   EZLDA_E_INVALID = 1, /* bad argument: n_tokens = 0, K = 0, alpha <= 0, beta <= 0, id out of range, NULL */
-  EZLDA_E_RANGE = 2,   /* packing limit exceeded: K, doc length, tokens per shard */
+  EZLDA_E_RANGE = 2,   /* packing limit exceeded: K, doc length, tokens per shard (>= 2^31) */
   EZLDA_E_NOMEM = 3,   /* device or host allocation failed */
   EZLDA_E_CUDA = 4,    /* CUDA runtime error (sticky) */
   EZLDA_E_NCCL = 5,    /* NCCL error or NCCL unavailable when world > 1 (sticky) */
@@ -92,8 +92,18 @@ typedef struct {
                              /* Any other value -> EZLDA_E_INVALID.                             */
   uint64_t local_group;      /* test hook, world > 1: nonzero key = the ranks are handles of */
                              /* THIS process on one device (one host thread per rank); the  */
-                             /* W / n_k merge is an in-process device sum instead of NCCL   */
+                             /* W / n_k merge is an in-process device sum instead of NCCL.  */
+                             /* Every rank of a key must pass the same world (else E_INVALID)*/
+  uint32_t debug_flags;      /* test hooks forcing rarely taken paths (EZLDA_DEBUG_*); the   */
+                             /* topics do not depend on them                                */
 } ezlda_options;
+
+/* debug_flags bits.  NO_TAIL_ROWS: word-prep precomputes the fixed-point rows of the dense
+ * words only, so every tail-word item is staged by a sampler warp (the path large V x K
+ * shards take when the rows do not fit).  C1_LOOKUP: the doc pass never carries C1 in the
+ * z^i marker, so every sampled token looks C1 up in the packed D row (the path of
+ * C1 >= 0x7FFF). */
+enum { EZLDA_DEBUG_NO_TAIL_ROWS = 1u, EZLDA_DEBUG_C1_LOOKUP = 2u };
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL
  * to query nnz (row_ptr may also be NULL then).  row_ptr has rows+1 entries. */
@@ -148,8 +158,9 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters);
  *   W: V rows in original word ids (or NULL); D: n_docs rows (or NULL). */
 ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W, ezlda_csr* D);
 
-/* Replace the state with caller topics (input order, each < K) as if `iterations_done`
- * iterations had completed (resume / test hook).  Rebuilds W and n_k. */
+/* Replace the state with caller topics (input order, each < K; host or device memory) as if
+ * `iterations_done` iterations had completed (resume / test hook).  Rebuilds W and n_k.
+ * A topic >= K returns EZLDA_E_INVALID and leaves the state unchanged. */
 ezlda_status ezlda_set_topics(ezlda* h, const uint16_t* topics, uint32_t iterations_done);
 
 /* Log-likelihood per token, Eq (5), log2, of the current state; for

@@ -411,6 +411,14 @@ static void what_row(const ezlda_oracle* h, const int32_t* W, const double* den,
   for (uint32_t k = 0; k < h->K; ++k) row[k] = ((double)W[(size_t)v * h->K + k] + h->beta) / den[k];
 }
 
+void ezlda_oracle_what_row(const int32_t* W_row, const int32_t* n_k, uint32_t K, uint32_t V, double beta,
+                           double* row) {
+  for (uint32_t k = 0; k < K; ++k) {
+    const double den = (double)n_k[k] + (double)V * beta;
+    row[k] = ((double)W_row[k] + beta) / den;
+  }
+}
+
 int ezlda_oracle_what(const ezlda_oracle* h, uint32_t v, const int32_t* W_global, const int32_t* nk_global,
                       double* row) {
   if (v >= h->V) return 1;

@@ -91,6 +91,10 @@ uint32_t ezlda_oracle_iterations(const ezlda_oracle* h);
  * W_global/nk_global override the snapshot as in iterate (may be NULL). */
 int ezlda_oracle_what(const ezlda_oracle* h, uint32_t v, const int32_t* W_global, const int32_t* nk_global,
                       double* row);
+/* What row of one word from its count row: row[k] = (W_row[k] + beta) / (n_k[k] + V beta)
+ * (Eq 1-2; the same expression what_row applies inside the chain). */
+void ezlda_oracle_what_row(const int32_t* W_row, const int32_t* n_k, uint32_t K, uint32_t V, double beta,
+                           double* row);
 /* Sampler of the chain: 3 = three-branch (default), 2 = two-branch ESCA
  * (ezlda_oracle_draw_two_branch per token, no skip test, Alg P:1481-1507).
  * last_stats then reports skip_S = skip_final = 0 and branch_hist[2] / [3] = S / Q draws. */

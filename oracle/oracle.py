@@ -68,6 +68,9 @@ def lib():
                                                    C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
                                                    P(C.c_double), P(C.c_double)]
         L.ezlda_oracle_draw_two_branch.restype = C.c_uint32
+        L.ezlda_oracle_what_row.argtypes = [P(C.c_int32), P(C.c_int32), C.c_uint32, C.c_uint32, C.c_double,
+                                            P(C.c_double)]
+        L.ezlda_oracle_what_row.restype = None
         L.ezlda_oracle_set_sampler.argtypes = [C.c_void_p, C.c_uint32]
         L.ezlda_oracle_set_sampler.restype = C.c_int
         L.ezlda_oracle_inverted_index.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32,
@@ -135,6 +138,15 @@ def draw_grid(Drow, What, alpha: float, g: int, u) -> tuple[np.ndarray, np.ndarr
     if rc:
         raise ValueError(f"ezlda_oracle_draw_grid rc={rc}")
     return topics, branch
+
+
+def what_row(W_row, n_k, V: int, beta: float) -> np.ndarray:
+    """What[v][.] = (W[v][.] + beta) / (n_k + V beta) from a count row (Eq 1-2)."""
+    Wr = np.ascontiguousarray(W_row, dtype=np.int32)
+    nk = np.ascontiguousarray(n_k, dtype=np.int32)
+    row = np.zeros(len(Wr))
+    lib().ezlda_oracle_what_row(_ptr(Wr, C.c_int32), _ptr(nk, C.c_int32), len(Wr), V, beta, _ptr(row, C.c_double))
+    return row
 
 
 def draw_two_branch(Drow, What, alpha: float, u: float) -> dict:

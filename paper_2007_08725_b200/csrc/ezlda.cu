@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <condition_variable>
 #include <cub/cub.cuh>
 #include <map>
@@ -71,6 +72,14 @@ __global__ void k_max_u32(const uint32_t* a, uint64_t n, uint32_t* out) {
   uint32_t m = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     m = max(m, a[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+__global__ void k_max_u16(const uint16_t* a, uint64_t n, uint32_t* out) {
+  uint32_t m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, (uint32_t)a[i]);
   for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
@@ -208,6 +217,7 @@ inline unsigned blocks(uint64_t n, unsigned t = 256) { return (unsigned)((n + t 
 // ----------------------------------------------------------------------------
 struct ezlda {
   void* lgroup = nullptr;  // LocalGroup* of the in-process rank group (options.local_group), else NCCL
+  uint64_t lgroup_key = 0;
   bool multi = false;      // multi-rank path: world > 1, or a one-rank NCCL group (world == 1 + nccl id)
   Dev dev{};
   Buf buf[2]{};
@@ -246,6 +256,7 @@ struct ezlda {
   ezl::Counters* ctr_host = nullptr;  // pinned, kSlots entries
   uint32_t exact_all = 0;             // options.exact_draws
   uint32_t branches = 3;              // options.sampler (2: two-branch ESCA mode)
+  uint32_t debug_flags = 0;           // options.debug_flags (EZLDA_DEBUG_*)
   ezlda_iter_stats sum{};
   uint32_t sum_n = 0;
   double* llpt_partial = nullptr;
@@ -323,22 +334,39 @@ ezlda_status cub_call(ezlda* h, F f) {
 struct LocalGroup {
   std::mutex m;
   std::condition_variable cv;
-  int world = 0, arrived = 0, left = 0;
+  int world = 0, arrived = 0, members = 0;
   uint64_t gen = 0;
+  bool broken = false;  // a barrier timed out: every later barrier fails at once
   std::vector<const void*> bufs;
 };
 std::mutex g_groups_m;
 std::map<uint64_t, LocalGroup*> g_groups;
 
-LocalGroup* local_group(uint64_t key, int world) {
+// Join the group of `key` (created by its first member with `world` ranks); nullptr if the
+// key already names a group with a different world.
+LocalGroup* local_group_join(uint64_t key, int world) {
   std::lock_guard<std::mutex> lk(g_groups_m);
   LocalGroup*& g = g_groups[key];
   if (!g) {
     g = new LocalGroup();
     g->world = world;
     g->bufs.assign(world, nullptr);
+  } else if (g->world != world) {
+    return nullptr;
   }
+  g->members += 1;
   return g;
+}
+
+// Leave the group; the last member frees it (the key can then be reused with any world).
+void local_group_leave(uint64_t key) {
+  std::lock_guard<std::mutex> lk(g_groups_m);
+  auto it = g_groups.find(key);
+  if (it == g_groups.end()) return;
+  if (--it->second->members == 0) {
+    delete it->second;
+    g_groups.erase(it);
+  }
 }
 
 template <typename T>
@@ -350,17 +378,24 @@ __global__ void k_sum_ranks(const T* const* src, int n, size_t count, T* dst) {
   }
 }
 
-// barrier of the group; phase = number of completed barriers of this handle
-void group_barrier(LocalGroup* g) {
+// Barrier of the group.  A rank that failed never arrives: the others give up after 600 s
+// (and the group is marked broken) instead of blocking forever.
+bool group_barrier(LocalGroup* g) {
   std::unique_lock<std::mutex> lk(g->m);
+  if (g->broken) return false;
   const uint64_t my = g->gen;
   if (++g->arrived == g->world) {
     g->arrived = 0;
     ++g->gen;
     g->cv.notify_all();
-  } else {
-    g->cv.wait(lk, [&] { return g->gen != my; });
+    return true;
   }
+  if (!g->cv.wait_for(lk, std::chrono::seconds(600), [&] { return g->gen != my || g->broken; }) || g->broken) {
+    g->broken = true;
+    g->cv.notify_all();
+    return false;
+  }
+  return true;
 }
 
 ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
@@ -371,7 +406,7 @@ ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t d
     std::lock_guard<std::mutex> lk(g->m);
     g->bufs[h->rank] = buf;
   }
-  group_barrier(g);  // every rank's buffer is final and registered
+  if (!group_barrier(g)) return h->fail(EZLDA_E_STATE, "local group barrier timed out (a rank failed)");
   void* tmp = nullptr;
   EZ_CUDA(h, cudaMalloc(&tmp, count * esz + sizeof(void*) * g->world));
   const void** d_src = reinterpret_cast<const void**>(static_cast<char*>(tmp) + count * esz);
@@ -388,7 +423,7 @@ ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t d
     k_sum_ranks<double><<<nb, 256, 0, h->stream>>>(reinterpret_cast<const double* const*>(d_src), g->world, count,
                                                    static_cast<double*>(tmp));
   EZ_CUDA(h, cudaStreamSynchronize(h->stream));
-  group_barrier(g);  // every rank has read every buffer
+  if (!group_barrier(g)) return h->fail(EZLDA_E_STATE, "local group barrier timed out (a rank failed)");
   EZ_CUDA(h, cudaMemcpyAsync(buf, tmp, count * esz, cudaMemcpyDeviceToDevice, h->stream));
   EZ_CUDA(h, cudaStreamSynchronize(h->stream));
   cudaFree(tmp);
@@ -414,6 +449,7 @@ void fill_dev(ezlda* h) {
   d.rs = ezl::wrow_stride(h->K);
   d.segw = ezl::seg_width(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
+  d.c1_cap = (h->debug_flags & EZLDA_DEBUG_C1_LOOKUP) ? 0u : 0x7FFFu;
   {
     const ezl::SamplerLayout L = ezl::sampler_layout(h->K);
     d.nslots = L.nslots;
@@ -752,6 +788,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
     const uint64_t budget = std::min<uint64_t>(32ull << 30, fr / 4);
     d.Vw = ((uint64_t)h->V * d.rs * 8ull <= budget) ? h->V : h->Vd;
+    if (o.debug_flags & EZLDA_DEBUG_NO_TAIL_ROWS) d.Vw = h->Vd;  // tail rows staged by a sampler warp
     if (h->branches == 2) d.Vw = 0;  // the two-branch mode does not use the three-branch records
   }
   EZ_ALLOC(h, d.wrow, double, (size_t)d.Vw * d.rs);
@@ -782,15 +819,14 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(d_L);
   h->release(d_cnt);
   h->release(d_max);
-  EZ_CUDA(h, ezl::configure_kernels(h->K));
+  EZ_CUDA(h, ezl::configure_kernels(h->K, &d.sampler_grid));
   {  // per-(sampler block, slot) scratch: HBM histograms (large K) and exact Q' tables of
      // warp-staged tail rows
-    const size_t n = (size_t)ezl::sampler_grid_size() * d.nslots * d.Kpad;
-    const size_t nh = (size_t)ezl::sampler_grid_size() * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
+    const size_t nh = (size_t)d.sampler_grid * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
     EZ_ALLOC(h, d.hist_scratch, uint32_t, nh);
     EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
     EZ_ALLOC(h, d.qp_scratch, double,
-             (size_t)ezl::sampler_grid_size() * d.nslots * ezl::sampler_qp_scratch_stride(d.Kpad));
+             (size_t)d.sampler_grid * d.nslots * ezl::sampler_qp_scratch_stride(d.Kpad));
   }
   // ---- iteration 0
   h->cur = 0;
@@ -898,7 +934,8 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   if (K > 65535) return bad(EZLDA_E_RANGE, "K > 65535 (16-bit topic packing, P:753)");
   if (K > 16384 || ezl::sampler_slots(K) == 0)
     return bad(EZLDA_E_RANGE, "K > 16384 not supported by this build (14-bit topic field of the packed D entries)");
-  if (n_tokens >= (1ull << 32)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^32 per shard");
+  // the setup sorts and scans (CUB) index the shard's tokens with int
+  if (n_tokens >= (1ull << 31)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^31 per shard");
   ezlda_options o{};
   if (opts) {  // struct_size versioning: a smaller (older) struct leaves the new fields zero
     const size_t n = opts->struct_size ? std::min<size_t>(opts->struct_size, sizeof(o)) : sizeof(o);
@@ -924,6 +961,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   h->timing = !o.no_phase_timing;
   h->exact_all = o.exact_draws ? 1u : 0u;
   h->branches = o.sampler ? o.sampler : 3u;
+  h->debug_flags = o.debug_flags;
   h->dev.token_base = o.token_base;
   ezlda_status st = EZLDA_OK;
   if (o.stream) {
@@ -938,7 +976,10 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   }
   if (h->multi && o.local_group) {
     if (o.rank < 0 || o.rank >= h->world) st = h->fail(EZLDA_E_INVALID, "local_group needs 0 <= rank < world");
-    else h->lgroup = local_group(o.local_group, h->world);
+    else if (!(h->lgroup = local_group_join(o.local_group, h->world)))
+      st = h->fail(EZLDA_E_INVALID, "local_group key %llu is in use with a different world",
+                   (unsigned long long)o.local_group);
+    else h->lgroup_key = o.local_group;
   } else if (h->multi) {
     if (!o.nccl_unique_id || o.rank < 0 || o.rank >= h->world) {
       st = h->fail(EZLDA_E_INVALID, "world >= 1 with NCCL needs nccl_unique_id and 0 <= rank < world");
@@ -1113,17 +1154,21 @@ ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W
 ezlda_status ezlda_set_topics(ezlda* h, const uint16_t* topics, uint32_t iterations_done) {
   if (!h || !topics) return EZLDA_E_INVALID;
   if (h->sticky) return EZLDA_E_STATE;
-  std::vector<uint16_t> tmp_h;
-  cudaPointerAttributes attr{};
-  const bool on_dev = cudaPointerGetAttributes(&attr, topics) == cudaSuccess && attr.type == cudaMemoryTypeDevice;
-  cudaGetLastError();
-  if (!on_dev) {
-    for (uint64_t t = 0; t < h->N; ++t)
-      if (topics[t] >= h->K) return h->fail(EZLDA_E_INVALID, "topic %u >= K at token %llu", topics[t], (unsigned long long)t);
-  }
   uint16_t* tmp = h->alloc<uint16_t>(h->N);
-  if (!tmp) return h->fail(EZLDA_E_NOMEM, "topics staging");
+  uint32_t* d_max = h->alloc<uint32_t>(1);
+  if (!tmp || !d_max) return h->fail(EZLDA_E_NOMEM, "topics staging");
   EZ_CUDA(h, cudaMemcpyAsync(tmp, topics, sizeof(uint16_t) * h->N, cudaMemcpyDefault, h->stream));
+  // validate on the device (host or device input alike) before anything is replaced
+  EZ_CUDA(h, cudaMemsetAsync(d_max, 0, 4, h->stream));
+  k_max_u16<<<1184, 256, 0, h->stream>>>(tmp, h->N, d_max);
+  uint32_t mx = 0;
+  EZ_CUDA(h, cudaMemcpyAsync(&mx, d_max, 4, cudaMemcpyDeviceToHost, h->stream));
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  h->release(d_max);
+  if (mx >= h->K) {
+    h->release(tmp);
+    return h->fail(EZLDA_E_INVALID, "topic %u >= K = %u", mx, h->K);
+  }
   ezl::launch_topics_from_input(tmp, h->perm, (uint32_t)h->N, h->buf[h->cur].z, h->stream);
   EZ_CUDA(h, cudaGetLastError());
   ezlda_status st = rebuild_counts(h);
@@ -1187,6 +1232,7 @@ void ezlda_destroy(ezlda* h) {
     for (auto& e : sl.ev)
       if (e) cudaEventDestroy(e);
   if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  if (h->lgroup) local_group_leave(h->lgroup_key);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

@@ -16,6 +16,8 @@
 //                                                                                  P:822-846)
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "kernels.h"
 
@@ -460,7 +462,7 @@ __device__ __forceinline__ void mpt_token(const Dev& d, const Buf& nxt, uint32_t
     ++n_skip;
   } else {
     // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
-    nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, 0x7FFFu)) : kUnsampled;
+    nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, d.c1_cap)) : kUnsampled;
     atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
   }
 }
@@ -485,7 +487,7 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
       ++n_skip;
     } else {
       // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
-      nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, 0x7FFFu)) : kUnsampled;
+      nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, d.c1_cap)) : kUnsampled;
       const uint32_t rid = d.trid[j];
       atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
     }
@@ -1045,7 +1047,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (d.zmark) {
       if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
       C1 = zm & 0x7FFFu;
-      if (C1 == 0x7FFFu) C1 = row_count(E, s_nnz, K1);
+      if (C1 == d.c1_cap) C1 = row_count(E, s_nnz, K1);  // saturated marker: look C1 up
     } else {
       if (zm != kUnsampled) continue;
       C1 = row_count(E, s_nnz, K1);
@@ -1852,7 +1854,6 @@ bool two_branch_word_major(uint32_t K) { return tb_item_smem_bytes(K) <= 200u * 
 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
-static uint32_t g_sampler_grid = 0;  // SMs x resident sampler blocks (configure_kernels)
 static const void* sampler_kernel(uint32_t segw, uint32_t qg) {
   switch (segw) {  // K <= 16384: segment widths 8 .. 64
     case 8u: return qg ? (const void*)k_sampler<8u, true> : (const void*)k_sampler<8u, false>;
@@ -1861,40 +1862,47 @@ static const void* sampler_kernel(uint32_t segw, uint32_t qg) {
     default: return qg ? (const void*)k_sampler<64u, true> : (const void*)k_sampler<64u, false>;
   }
 }
-static uint32_t sampler_grid() { return g_sampler_grid ? g_sampler_grid : 148u; }
-uint32_t sampler_grid_size() { return sampler_grid(); }
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
 
 size_t word_prep_smem_bytes(uint32_t K) { return (size_t)kWpWarps * ((K + 31) / 32) * 32 * 8; }  // row per warp
 
-cudaError_t configure_kernels(uint32_t K) {
+// The dynamic shared-memory limit of a kernel is process-wide state of the device: it is
+// only ever RAISED here (to the largest size any live or past handle asked for), so a handle
+// with a small K never invalidates the launches of a live handle with a large K.
+static std::mutex g_attr_m;
+static std::map<std::pair<int, const void*>, int> g_attr;  // (device, kernel) -> limit set
+
+static cudaError_t raise_smem(int dev, const void* k, int bytes) {
+  int& cur = g_attr[{dev, k}];
+  if (bytes <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
+cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
+  std::lock_guard<std::mutex> lk(g_attr_m);
   cudaError_t e;
-  if (K <= kWpSmallK &&
-      (e = cudaFuncSetAttribute(k_word_prep_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)word_prep_smem_bytes(K))))
-    return e;
+  int dev = 0, nsm = 0, nb = 0;
+  if ((e = cudaGetDevice(&dev))) return e;
+  if (K <= kWpSmallK && (e = raise_smem(dev, (const void*)k_word_prep_w, (int)word_prep_smem_bytes(K)))) return e;
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
-  if ((e = cudaFuncSetAttribute(k_llpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)llpt_smem_bytes(K)))) return e;
-  {
-    const void* ks = sampler_kernel(seg_width(K), sampler_layout(K).qfx_global);
-    if ((e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, sp))) return e;
-    int dev = 0, nsm = 0, nb = 0;
-    if ((e = cudaGetDevice(&dev))) return e;
-    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks, kSampWarpsP * 32, (size_t)sp))) return e;
-    if (nb < 1) return cudaErrorInvalidConfiguration;
-    g_sampler_grid = (uint32_t)(nsm * nb);
-  }
-  if ((e = cudaFuncSetAttribute(k_wcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wcount_smem_bytes(K))))
+  if ((e = raise_smem(dev, (const void*)k_llpt, (int)llpt_smem_bytes(K)))) return e;
+  const void* ks = sampler_kernel(seg_width(K), sampler_layout(K).qfx_global);
+  if ((e = raise_smem(dev, ks, sp))) return e;
+  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks, kSampWarpsP * 32, (size_t)sp))) return e;
+  if (nb < 1) return cudaErrorInvalidConfiguration;
+  *grid = (uint32_t)(nsm * nb);
+  if ((e = raise_smem(dev, (const void*)k_wcount, (int)wcount_smem_bytes(K)))) return e;
+  if (two_branch_word_major(K) && (e = raise_smem(dev, (const void*)k_tb_item, (int)tb_item_smem_bytes(K))))
     return e;
-  if (two_branch_word_major(K) &&
-      (e = cudaFuncSetAttribute(k_tb_item, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb_item_smem_bytes(K))))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_doc_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
-  if ((e = cudaFuncSetAttribute(k_doc_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, db))) return e;
+  if ((e = raise_smem(dev, (const void*)k_doc_block<false>, db))) return e;
+  if ((e = raise_smem(dev, (const void*)k_doc_block<true>, db))) return e;
   if (K <= 4096) {
     const int dh = kDocWarps * (int)(((K + 31) / 32) * 17) * 4;
-    if ((e = cudaFuncSetAttribute(k_doc_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
-    if ((e = cudaFuncSetAttribute(k_doc_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dh))) return e;
+    if ((e = raise_smem(dev, (const void*)k_doc_hist<false>, dh))) return e;
+    if ((e = raise_smem(dev, (const void*)k_doc_hist<true>, dh))) return e;
   }
   return cudaSuccess;
 }
@@ -1943,7 +1951,7 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
   else
     {
       const void* ks = sampler_kernel(d.segw, d.qfx_global);
-      const uint32_t grid = std::min<uint32_t>(n_items, sampler_grid());
+      const uint32_t grid = std::min<uint32_t>(n_items, d.sampler_grid);
       void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
       cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);
     }

@@ -64,7 +64,10 @@ struct Dev {
   double* tbw;         // two-branch mode: [V * Kpad] What rows (Eq 1-2)
   double* tbq;         // two-branch mode: [V * Kpad] Q tree prefix sum_{j<=k} alpha What_j
   uint32_t Vw;     // words v < Vw have their What' | QP row precomputed in wrow (Vd, or V if it fits)
-  uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, 0x7FFF)
+  uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, c1_cap)
+  uint32_t c1_cap; // 0x7FFF; a marker equal to it sends the sampler to the packed-row lookup of C1 (debug
+                   // flag EZLDA_DEBUG_C1_LOOKUP sets it to 0: every failing token takes the lookup)
+  uint32_t sampler_grid;  // persistent sampler grid of this handle (SMs x resident blocks, configure_kernels)
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
   uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
   double alpha, beta, Vbeta;
@@ -132,11 +135,12 @@ struct SamplerLayout {
   size_t smem_bytes;
 };
 SamplerLayout sampler_layout(uint32_t K);
-uint32_t sampler_grid_size();  // persistent sampler grid (after configure_kernels)
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad);  // doubles per slot of qp_scratch
 uint32_t wrow_stride(uint32_t K);
 uint32_t seg_width(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);
-cudaError_t configure_kernels(uint32_t K);
+// Raise the dynamic shared-memory limits of the kernels K needs (never lowered: handles with
+// different K may be alive at once) and return this K's persistent sampler grid in *grid.
+cudaError_t configure_kernels(uint32_t K, uint32_t* grid);
 
 }  // namespace ezl

@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("EZLDA_LIB") or os.path.join(HERE, "libezlda.so")
 
 EZLDA_W_HYBRID, EZLDA_W_ALL_DENSE, EZLDA_W_ALL_SPARSE = 0, 1, 2
+EZLDA_DEBUG_NO_TAIL_ROWS, EZLDA_DEBUG_C1_LOOKUP = 1, 2
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_RANGE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_NCCL", 6: "E_STATE"}
 
 # every symbol include/ezlda.h declares
@@ -29,6 +30,7 @@ class Options(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("token_base", C.c_uint64), ("stream", C.c_void_p),
         ("input_on_device", C.c_uint32), ("no_phase_timing", C.c_uint32), ("doc_block_kb", C.c_uint32),
         ("exact_draws", C.c_uint32), ("sampler", C.c_uint32), ("local_group", C.c_uint64),
+        ("debug_flags", C.c_uint32),
     ]
 
 
@@ -115,7 +117,7 @@ class EzLDA:
                  dense_threshold: int = 0, split_threshold: int = 0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, token_base: int = 0, stream: int | None = None,
                  phase_timing: bool = True, doc_block_kb: int = 0, exact_draws: bool = False,
-                 local_group: int = 0, sampler: int = 3):
+                 local_group: int = 0, sampler: int = 3, debug_flags: int = 0):
         L = load()
         self._h = None
         on_dev = bool(getattr(word_ids, "is_cuda", False))
@@ -140,6 +142,7 @@ class EzLDA:
         o.exact_draws = 1 if exact_draws else 0
         o.local_group = local_group
         o.sampler = sampler  # 3: three-branch (default), 2: two-branch ESCA baseline mode
+        o.debug_flags = debug_flags  # EZLDA_DEBUG_* test hooks (rarely taken paths; same topics)
         h = C.c_void_p()
         rc = L.ezlda_create(_addr(word_ids), _addr(doc_ids), self.N, self.n_docs, self.V, self.K, self.alpha,
                             self.beta, seed, C.byref(o), C.byref(h))

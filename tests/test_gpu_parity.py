@@ -5,9 +5,9 @@ GPU's z^{i-1}; both run iteration i with the same Philox stream, and the GPU's
 integer D / W / n_k must equal a brute-force recount of its own topics bit for bit.
 Topics: the north star's bar is >= 99.99% agreement with every disagreement at a bucket
 boundary (checked: within 1e-12 Z).  The CUDA path is built to meet a stronger bar -- its
-fp32 fast path only keeps decisions certified by an error margin and redraws the others
-with the oracle's fp64 operations and orders -- so the tests also
-require ZERO disagreements (bit-identical topics).
+fast path sums exact 64-bit fixed-point products and keeps only decisions certified by an
+error margin, redrawing the others with the oracle's fp64 operations and orders (DESIGN.md
+section 2) -- so the tests also require ZERO disagreements (bit-identical topics).
 """
 import numpy as np
 import pytest
@@ -59,6 +59,13 @@ def check_counts(ez, g, w, d, n_docs, V, K, z=None):
     for r in range(0, n_docs, max(1, n_docs // 50)):
         c = col[rp[r]:rp[r + 1]]
         assert np.all(np.diff(c.astype(np.int64)) > 0)
+
+
+def oracle_chain(oracle_mod, w, d, n_docs, V, K, iters, sampler=3, **kw):
+    """The oracle's own chain (independent of the GPU): topics / n_k / LLPT after `iters`."""
+    orc = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=SAMPLER_SEED, branches=sampler, **kw)
+    orc.iterate(iters)
+    return orc
 
 
 def boundary_distance(oracle_mod, orc, w, d, z_prev, t, K, alpha, g, it):
@@ -117,7 +124,7 @@ def run_one_step_parity(ez, oracle_mod, w, d, n_docs, V, K, iters, g=2, check_ev
         z = zg
     print(f"worst per-iteration agreement {worst:.6f}, total mismatches {total_mismatch}, "
           f"exact redraws (last iteration) {gpu.stats()['exact_redraws']}")
-    assert total_mismatch == 0, "fp32 fast path + exact redraw must reproduce the oracle's topics bit for bit"
+    assert total_mismatch == 0, "certified fast path + exact redraw must reproduce the oracle's topics bit for bit"
     return gpu, orc
 
 
@@ -154,7 +161,7 @@ def test_large_K_paths(ez, oracle_mod, K):
 
 def test_exact_draws_knob_identical(ez, oracle_mod, small):
     """exact_draws=1 sends every sampled token through the fp64 path: topics identical to
-    the default fp32-certified path and to the oracle; the default path redraws few tokens."""
+    the default certified fixed-point path and to the oracle; the default path redraws few tokens."""
     w, d = small
     K = 64
     a = ez.EzLDA(w, d, SMALL["n_docs"], SMALL["V"], K, seed=SAMPLER_SEED)
@@ -224,16 +231,21 @@ def test_appendix_a_state_loglik(ez):
     dict(split_threshold=64, w_mode=1), dict(g=1), dict(g=3), dict(doc_block_kb=1),
     dict(doc_block_kb=1, split_threshold=100),
 ])
-def test_knob_invariance(ez, tiny, knobs):
-    """Dense threshold, W mode, region split and g change speed only: T bit-identical."""
+def test_knob_invariance(ez, oracle_mod, tiny, knobs):
+    """Dense threshold, W mode, region split, doc windows and g change speed only: T
+    bit-identical to the default GPU chain AND to the oracle's chain, every iteration."""
     w, d = tiny
     ref = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED)
     alt = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED, **knobs)
+    orc = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED, g=knobs.get("g", 2))
     for _ in range(6):
         ref.iterate(1)
         alt.iterate(1)
+        orc.iterate(1)
+        assert np.array_equal(alt.topics(), orc.topics()), knobs
         assert np.array_equal(ref.topics(), alt.topics()), knobs
     assert np.array_equal(ref.n_k(), alt.n_k())
+    assert np.array_equal(alt.n_k(), orc.counts()[2])
 
 
 def test_determinism(ez, small):
@@ -292,7 +304,7 @@ def test_invalid_arguments(ez):
 
 @pytest.mark.parametrize("sampler", [3, 2])
 @pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_library_path_one_gpu(ez, world, sampler):
+def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler):
     """The library's multi-rank path (doc shards with token bases, global word counts and
     relabelling, all-dense W merged every iteration, LLPT reduction) with the ranks as
     handles of this process on one GPU (options.local_group: the merge is an in-process
@@ -329,6 +341,12 @@ def test_multi_rank_library_path_one_gpu(ez, world, sampler):
     assert not errs, errs
     z = np.concatenate([out[r][0] for r in range(world)])
     assert np.array_equal(z, z_ref)
+    # ... and equal the oracle's chain (independent of the GPU)
+    orc = oracle_chain(oracle_mod, w, d, n_docs, V, K, iters, sampler)
+    assert np.array_equal(z, orc.topics())
+    _, W_orc, nk_orc = orc.counts()
+    assert np.array_equal(nk_ref, nk_orc) and np.array_equal(W_ref, W_orc)
+    assert abs(ll_ref - orc.loglik(1)) <= 1e-10 * abs(ll_ref)
     for r in range(world):
         assert np.array_equal(out[r][1], W_ref), r
         assert np.array_equal(out[r][2], nk_ref), r
@@ -374,7 +392,7 @@ def test_two_branch_mode_parity(ez, oracle_mod, case):
 
 
 @pytest.mark.parametrize("sampler", [3, 2])
-def test_checkpoint_resume_is_exact(ez, small, sampler):
+def test_checkpoint_resume_is_exact(ez, oracle_mod, small, sampler):
     """Checkpoint = (topics, iterations done) from ezlda_counts; resume = a fresh handle +
     ezlda_set_topics: the resumed chain equals the uninterrupted one bit for bit (the draws
     are keyed by (token, iteration))."""
@@ -391,10 +409,13 @@ def test_checkpoint_resume_is_exact(ez, small, sampler):
     assert np.array_equal(a.topics(), b.topics())
     assert np.array_equal(a.n_k(), b.n_k())
     assert a.loglik() == b.loglik()
+    orc = oracle_chain(oracle_mod, w, d, SMALL["n_docs"], SMALL["V"], K, 8, sampler)
+    assert np.array_equal(b.topics(), orc.topics())
+    assert abs(b.loglik() - orc.loglik(1)) <= 1e-10 * abs(orc.loglik(1))
 
 
 @pytest.mark.parametrize("sampler", [3, 2])
-def test_one_rank_nccl_group_matches_single_gpu(ez, sampler):
+def test_one_rank_nccl_group_matches_single_gpu(ez, oracle_mod, sampler):
     """world = 1 with an ncclUniqueId: the library's multi-rank path -- global word counts
     all-reduced at create, every W row dense, W and n_k merged by ncclAllReduce every
     iteration, LLPT reduced -- through a real one-rank NCCL communicator (the only NCCL
@@ -410,3 +431,77 @@ def test_one_rank_nccl_group_matches_single_gpu(ez, sampler):
     assert np.array_equal(ez.EzLDA.csr_to_dense(*h.W_csr(), K), ez.EzLDA.csr_to_dense(*ref.W_csr(), K))
     assert np.array_equal(h.n_k(), ref.n_k())
     assert h.loglik() == ref.loglik()
+    orc = oracle_chain(oracle_mod, w, d, n_docs, V, K, iters, sampler)
+    assert np.array_equal(h.topics(), orc.topics())
+    assert np.array_equal(h.n_k(), orc.counts()[2])
+
+
+DEBUG_CASES = {
+    # every tail-word item staged by a sampler warp (stage_tail_row_warp + per-slot QP scratch)
+    "no_tail_rows_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 3, 1),
+    "no_tail_rows_K64": (SMALL, 64, 3, 1),
+    "no_tail_rows_K16384": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 16384, 2, 1),
+    # C1 never carried in the z^i marker: every sampled token looks C1 up in its packed D row
+    "c1_lookup_K64": (SMALL, 64, 3, 2),
+    "c1_lookup_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 2, 2),
+    "both_K5000": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 5000, 2, 3),
+}
+
+
+@pytest.mark.parametrize("case", list(DEBUG_CASES))
+def test_rare_paths_parity(ez, oracle_mod, case):
+    """Paths the default configs rarely or never take, forced by ezlda_options.debug_flags:
+    one-step parity with the oracle, bit-identical topics and exact counts."""
+    spec, K, iters, flags = DEBUG_CASES[case]
+    w, d = planted_corpus_np(**spec)
+    run_one_step_parity(ez, oracle_mod, w, d, spec["n_docs"], spec["V"], K, iters, check_every=iters,
+                        debug_flags=flags)
+
+
+def test_live_handles_with_different_K(ez, oracle_mod, tiny):
+    """Two live handles with different K (different sampler layouts / grids / shared-memory
+    sizes) iterated alternately: each equals its oracle chain (per-handle grid,
+    shared-memory limits only raised)."""
+    w, d = tiny
+    big = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16384, seed=SAMPLER_SEED)
+    small_ = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 64, seed=SAMPLER_SEED)
+    ob = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 16384, seed=SAMPLER_SEED)
+    os_ = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 64, seed=SAMPLER_SEED)
+    for _ in range(3):
+        small_.iterate(1)
+        big.iterate(1)
+        ob.iterate(1)
+        os_.iterate(1)
+        assert np.array_equal(big.topics(), ob.topics())
+        assert np.array_equal(small_.topics(), os_.topics())
+
+
+def test_set_topics_validates_device_input(ez, tiny):
+    """A topic >= K passed in DEVICE memory is rejected (E_INVALID) before any state change."""
+    import torch
+
+    w, d = tiny
+    g = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, seed=SAMPLER_SEED)
+    g.iterate(1)
+    z0 = g.topics()
+    bad = torch.from_numpy(z0.astype(np.int16)).cuda()
+    bad[17] = 16
+    with pytest.raises(ez.EzLDAError, match="E_INVALID"):
+        g.set_topics(bad, 5)
+    assert np.array_equal(g.topics(), z0)
+    ok = torch.from_numpy(z0.astype(np.int16)).cuda()
+    g.set_topics(ok, 1)
+    assert np.array_equal(g.topics(), z0)
+
+
+def test_local_group_world_mismatch_rejected(ez, tiny):
+    """A local_group key in use with another world is rejected; the key is reusable after the
+    group's handles are destroyed."""
+    w, d = tiny
+    n = len(w) // 2
+    a = ez.EzLDA(w[:n], d[:n], TINY["n_docs"], TINY["V"], 16, rank=0, world=2, local_group=777)
+    with pytest.raises(ez.EzLDAError, match="E_INVALID"):
+        ez.EzLDA(w[n:], d[n:], TINY["n_docs"], TINY["V"], 16, rank=1, world=3, local_group=777)
+    a.close()
+    b = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, rank=0, world=1, local_group=777)
+    b.close()

@@ -192,3 +192,34 @@ def test_two_branch_K1_all_zero(oracle_mod, tiny):
     assert not h.topics().any()
     with pytest.raises(ValueError):
         oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 4, branches=1)
+
+
+@pytest.mark.parametrize("branches, g", [(3, 2), (3, 1), (2, 2)])
+def test_iterate_is_per_token_draw_on_recounted_snapshot(oracle_mod, tiny, branches, g):
+    """Composition pin of the chain: every topic of one iterate() step equals the single-token
+    draw (draw_three_branch / draw_two_branch, pinned by Fig 2/4 and the brute-force u-measure)
+    applied to the recounted snapshot D[d], What[v] (numpy recount) with u = uniform(seed, i, t_g)
+    -- the snapshot semantics of SURVEY 8(c) steps 1-4."""
+    w, d = tiny
+    n_docs, V, K = TINY["n_docs"], TINY["V"], 16
+    seed = 5
+    h = oracle_mod.OracleLDA(w, d, n_docs, V, K, seed=seed, g=g, branches=branches)
+    h.iterate(2)
+    z_prev = h.topics()
+    i = h.iterations + 1
+    Db, Wb = brute_counts(w, d, z_prev, n_docs, V, K)
+    nk = Wb.sum(0)
+    tg = h.token_index()
+    h.iterate(1)
+    z_new = h.topics()
+    whats = {}
+    for t in range(len(w)):
+        v = int(w[t])
+        if v not in whats:
+            whats[v] = oracle_mod.what_row(Wb[v], nk, V, h.beta)
+        u = oracle_mod.uniform(seed, i, int(tg[t]))
+        if branches == 3:
+            topic = oracle_mod.draw_three_branch(Db[d[t]], whats[v], h.alpha, g, u)["topic"]
+        else:
+            topic = oracle_mod.draw_two_branch(Db[d[t]], whats[v], h.alpha, u)["topic"]
+        assert topic == z_new[t], (t, topic, z_new[t])

@@ -101,3 +101,13 @@ def test_fig5_inverted_index(oracle_mod):
     ofs, pos = oracle_mod.inverted_index(w, d, 3)
     got = [list(pos[ofs[i]:ofs[i + 1]]) for i in range(3)]
     assert got == [f5["doc0"], f5["doc1"], f5["doc2"]]
+
+
+def test_fig2_what_row_primitive(oracle_mod):
+    """ezlda_oracle_what_row (used to feed full-size parity checks) on the printed Fig 2 state:
+    W[0] = {0,1,1,0}, n_k = {2,3,1,1}, V = 4, beta = 0.01 -> What[0] as printed (P:384), and
+    identical to the chain's own What row."""
+    g, h = fig2_state(oracle_mod)
+    row = oracle_mod.what_row(g["W0"], g["n_k"], g["V"], g["beta"])
+    np.testing.assert_allclose(row, g["what0"], atol=6e-5)
+    assert np.array_equal(row, h.what(0))
