@@ -137,6 +137,9 @@ typedef struct {
   uint64_t kernel_launches;  /* library kernels launched by the iteration                  */
   uint64_t exact_redraws;    /* sampled tokens redrawn on the exact fp64 path (fixed-point decision
                                 not certified by its error margin)      */
+  double exchange_bytes;     /* H7 collective payload of the iteration (world > 1): int32 all-  */
+                             /* reduce of the dense W block + n_k, u16 all-gather of the tail  */
+                             /* topics (output size); 0 when world == 1                        */
 } ezlda_iter_stats;
 
 /* Build the resident corpus and draw z^0 (iteration 0).

@@ -41,6 +41,7 @@ struct NcclApi {
   decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
   decltype(&ncclCommInitRank) CommInitRank = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
 };
@@ -57,9 +58,11 @@ NcclApi& nccl() {
       api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
       api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
       api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy &&
+               api.GetErrorString;
     }
   }
   return api;
@@ -234,6 +237,15 @@ struct ezlda {
   uint32_t g = 2;
   int rank = 0, world = 1;
   uint64_t N_global = 0;
+  // tail-W exchange (world > 1): every rank all-gathers the new topics of its
+  // tail-word tokens in word-major order; each rank rebuilds the global tail rows from them
+  uint32_t rt0 = 0;                 // first word-major run of a tail word
+  uint64_t tail_max = 0;            // max over ranks of the local tail-token count (gather slot)
+  uint16_t* tz_local = nullptr;     // [tail_max] this rank's tail topics, word-major
+  uint16_t* tz_all = nullptr;       // [world * tail_max] gathered
+  uint32_t* tail_run_tok = nullptr; // [R - rt0] word-major offset of a tail run's tokens in tz_local
+  uint32_t* tail_off = nullptr;     // [world * (Vt + 1)] per-rank prefix of local tail counts
+  double exchange_bytes = 0;        // collective payload per iteration
   uint32_t* docs_w = nullptr;
   uint32_t* docs_b = nullptr;
   uint32_t* perm = nullptr;
@@ -437,6 +449,61 @@ ezlda_status allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
   return EZLDA_OK;
 }
 
+ezlda_status local_allgather(ezlda* h, const void* send, void* recv, size_t bytes) {
+  LocalGroup* g = static_cast<LocalGroup*>(h->lgroup);
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  {
+    std::lock_guard<std::mutex> lk(g->m);
+    g->bufs[h->rank] = send;
+  }
+  if (!group_barrier(g)) return h->fail(EZLDA_E_STATE, "local group barrier timed out (a rank failed)");
+  for (int r = 0; r < g->world; ++r)
+    if (bytes)
+      EZ_CUDA(h, cudaMemcpyAsync(static_cast<char*>(recv) + (size_t)r * bytes, g->bufs[r], bytes,
+                                 cudaMemcpyDeviceToDevice, h->stream));
+  EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+  if (!group_barrier(g)) return h->fail(EZLDA_E_STATE, "local group barrier timed out (a rank failed)");
+  return EZLDA_OK;
+}
+
+// recv[r * bytes .. (r + 1) * bytes) = rank r's send (device buffers, every rank the same size)
+ezlda_status allgather(ezlda* h, const void* send, void* recv, size_t bytes) {
+  if (!h->multi) return EZLDA_OK;
+  if (h->lgroup) return local_allgather(h, send, recv, bytes);
+  if (bytes) EZ_NCCL(h, nccl().AllGather(send, recv, bytes, ncclUint8, h->comm, h->stream));
+  return EZLDA_OK;
+}
+
+// word-major copy of the tail tokens' topics: run r (a tail word's run) -> tz[tail_run_tok[r]..]
+__global__ void k_tail_gather(const uint32_t* run_j0, const uint16_t* run_len, const uint32_t* run_tok, uint32_t rt0,
+                              uint32_t R, const uint16_t* z, uint16_t* tz) {
+  const uint32_t r = rt0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) {
+    const uint32_t j0 = run_j0[r], n = run_len[r], o = run_tok[r - rt0];
+    for (uint32_t t = 0; t < n; ++t) tz[o + t] = z[j0 + t];
+  }
+}
+
+__global__ void k_tail_run_tok(const uint32_t* tokpre, uint32_t rt0, uint32_t R, uint32_t* out) {
+  const uint32_t r = rt0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) out[r - rt0] = tokpre[r] - tokpre[rt0];
+}
+
+// W tail (world > 1): every rank's word-major tail topics -> the global packed tail rows
+ezlda_status merge_tail(ezlda* h, Buf& b) {
+  if (!h->multi || h->Vt == 0) return EZLDA_OK;
+  if (h->R > h->rt0) {
+    k_tail_gather<<<(unsigned)((h->R - h->rt0 + 255) / 256), 256, 0, h->stream>>>(
+        h->dev.run_j0, h->dev.run_len, h->tail_run_tok, h->rt0, h->R, b.z, h->tz_local);
+    EZ_CUDA(h, cudaGetLastError());
+  }
+  ezlda_status st = allgather(h, h->tz_local, h->tz_all, 2ull * h->tail_max);
+  if (st) return st;
+  ezl::launch_tail_rebuild(h->dev, b, h->tz_all, h->tail_off, (uint32_t)h->world, h->tail_max, h->stream);
+  EZ_CUDA(h, cudaGetLastError());
+  return EZLDA_OK;
+}
+
 void fill_dev(ezlda* h) {
   Dev& d = h->dev;
   d.N = (uint32_t)h->N;
@@ -480,6 +547,7 @@ ezlda_status rebuild_counts(ezlda* h) {
   ezlda_status s;
   if ((s = allreduce(h, b.Wd, (size_t)h->Vd * h->K, ncclInt32))) return s;
   if ((s = allreduce(h, b.nk, h->K, ncclInt32))) return s;
+  if ((s = merge_tail(h, b))) return s;
   h->D_fresh = false;
   return EZLDA_OK;
 }
@@ -576,8 +644,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   if (o.w_mode == EZLDA_W_ALL_SPARSE) thr = 65535;  // tail counts must fit 16 bits
   uint32_t Vd = 0;
   while (Vd < h->V && (cnt[h->origword[Vd]] > thr || cnt[h->origword[Vd]] > 65535)) ++Vd;
-  // world > 1: W is merged by an int32 all-reduce of dense rows (tail all-gather: next round)
-  if (o.w_mode == EZLDA_W_ALL_DENSE || h->multi) Vd = h->V;
+  if (o.w_mode == EZLDA_W_ALL_DENSE) Vd = h->V;
   h->Vd = Vd;
   h->Vt = h->V - Vd;
   std::vector<uint32_t> tofs(h->Vt + 1, 0);
@@ -715,6 +782,40 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(r0s);
   h->release(d_ni);
   h->release(vs);
+  if (h->multi && h->Vt) {  // ---- tail-W exchange layout (static): word-major tail runs, per-rank counts
+    EZ_CUDA(h, cudaMemcpyAsync(&h->rt0, wrun + h->Vd, 4, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    EZ_ALLOC(h, h->tail_run_tok, uint32_t, std::max<uint32_t>(R - h->rt0, 1));
+    if (R > h->rt0) k_tail_run_tok<<<blocks(R - h->rt0), 256, 0, s>>>(tokpre, h->rt0, R, h->tail_run_tok);
+    std::vector<uint32_t> tc(h->Vt), tc_all((size_t)h->world * h->Vt);
+    for (uint32_t t = 0; t < h->Vt; ++t) tc[t] = cnt_local[h->origword[h->Vd + t]];
+    uint32_t *d_tc, *d_tc_all;
+    EZ_ALLOC(h, d_tc, uint32_t, h->Vt);
+    EZ_ALLOC(h, d_tc_all, uint32_t, (size_t)h->world * h->Vt);
+    EZ_CUDA(h, cudaMemcpyAsync(d_tc, tc.data(), 4ull * h->Vt, cudaMemcpyHostToDevice, s));
+    if ((st = allgather(h, d_tc, d_tc_all, 4ull * h->Vt))) return st;
+    EZ_CUDA(h, cudaMemcpyAsync(tc_all.data(), d_tc_all, 4ull * h->world * h->Vt, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    h->release(d_tc);
+    h->release(d_tc_all);
+    std::vector<uint32_t> off((size_t)h->world * (h->Vt + 1));
+    h->tail_max = 1;
+    for (int r = 0; r < h->world; ++r) {
+      uint64_t acc = 0;
+      for (uint32_t t = 0; t < h->Vt; ++t) {
+        off[(size_t)r * (h->Vt + 1) + t] = (uint32_t)acc;
+        acc += tc_all[(size_t)r * h->Vt + t];
+      }
+      off[(size_t)r * (h->Vt + 1) + h->Vt] = (uint32_t)acc;
+      h->tail_max = std::max<uint64_t>(h->tail_max, acc);
+    }
+    EZ_ALLOC(h, h->tail_off, uint32_t, off.size());
+    EZ_CUDA(h, cudaMemcpyAsync(h->tail_off, off.data(), 4ull * off.size(), cudaMemcpyHostToDevice, s));
+    EZ_ALLOC(h, h->tz_local, uint16_t, h->tail_max);
+    EZ_ALLOC(h, h->tz_all, uint16_t, (size_t)h->world * h->tail_max);
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+  }
+  if (h->multi) h->exchange_bytes = 4.0 * ((double)h->Vd * h->K + h->K) + 2.0 * h->world * (h->Vt ? h->tail_max : 0);
   h->release(tokpre);
   h->release(wrun);
   // order: hot-word items window-major, heavy first within a window; then the other items
@@ -856,6 +957,7 @@ ezlda_status fold_one(ezlda* h) {
   st.d_nnz = c.d_nnz;
   st.kernel_launches = sl.launches;
   st.exact_redraws = c.exact;
+  st.exchange_bytes = h->exchange_bytes;
   if (h->timing) {
     float a = 0, b = 0, cc = 0, dd = 0;
     EZ_CUDA(h, cudaEventElapsedTime(&a, sl.ev[0], sl.ev[1]));
@@ -900,6 +1002,7 @@ ezlda_status fold_one(ezlda* h) {
   S.model_bytes_docpass += st.model_bytes_docpass;
   S.kernel_launches += st.kernel_launches;
   S.exact_redraws += st.exact_redraws;
+  S.exchange_bytes += st.exchange_bytes;
   h->sum_n += 1;
   return EZLDA_OK;
 }
@@ -1042,8 +1145,11 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     }
     EZ_CUDA(h, cudaGetLastError());
     ezlda_status st;
+    // H7 (world > 1): int32 all-reduce of the dense block and n_k, all-gather of
+    // the tail topics + tail-row rebuild (integer sums: W is identical on every rank)
     if ((st = allreduce(h, nxt.Wd, (size_t)h->Vd * h->K, ncclInt32))) return st;
     if ((st = allreduce(h, nxt.nk, h->K, ncclInt32))) return st;
+    if ((st = merge_tail(h, nxt))) return st;
     EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaEventRecord(ev[4], s));
     sl.iteration = i;
@@ -1051,6 +1157,7 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     // word-major kernel, or What/Q tables + doc-major draw + W count
     sl.launches = 3u + (h->n_docs_w ? 1u : 0u) + (h->n_docs_b ? 1u : 0u) - (h->n_items ? 0u : 1u);
     if (h->branches == 2) sl.launches = ezl::two_branch_word_major(h->K) ? sl.launches - 1u : sl.launches + 1u;
+    if (h->multi && h->Vt) sl.launches += (h->R > h->rt0 ? 1u : 0u) + 1u;  // tail gather + tail rebuild
     h->pending.push_back(si);
     h->cur = 1 - h->cur;
     h->iteration = i;

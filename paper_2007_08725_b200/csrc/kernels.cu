@@ -760,8 +760,9 @@ struct RunCounters {
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | queue
-  unsigned long long* P;  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
+struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | run sums | queue
+  unsigned long long* P;  // fixed-point chunk sums / prefix checkpoints of the batch's runs (sample_batch)
+  unsigned long long* S;  // [32] fixed-point S' of each run of the batch (8/16-entry segments)
   uint32_t* q;            // queue of flagged runs
 };
 
@@ -967,11 +968,18 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   }
   // ---- B: lane per segment (kSegW entries, 16 = two 32-byte sectors); consecutive lanes
   //      read consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the
-  //      word's fixed-point What' row), combined by a segmented warp scan (+ carry across
-  //      rounds).  Checkpoints: kSec (kSegW = 16) keeps two per segment, P[2g] = P(before g)
-  //      + (first sector) and P[2g+1] = P(end of g), so a descent walks at most one sector;
-  //      otherwise P[g] = P(end of g).  S' = the run's last checkpoint.
+  //      word's fixed-point What' row).
+  //      kSegW <= 16 (kChunk): every lane stores the sums of its 8-entry chunks (sectors), P[c],
+  //      and adds its segment total to the run's S' (shared 64-bit atomic) -- no scan: the
+  //      rare S'-branch descent walks the chunk sums of its run (phase D).
+  //      kSegW >= 32: a segmented warp scan (+ carry across rounds) turns segment sums into
+  //      run prefixes P[g] = P(end of g); S' = the run's last one (binary-searched in D).
+  constexpr bool kChunk = kSegW <= 16u;
   constexpr bool kSec = kSegW == 16u;
+  if (kChunk) {
+    if (lane < nb) ws.S[lane] = 0ull;
+    __syncwarp();
+  }
   unsigned long long carry = 0ull;
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
     const uint32_t g = B0 + lane;
@@ -999,6 +1007,20 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         }
       }
     }
+    if (kChunk) {
+      if (g < T) {
+        if (kSec) {  // the two sector sums of the segment are adjacent: one 16-byte store
+          ulonglong2 pr;
+          pr.x = acc8;
+          pr.y = acc - acc8;
+          *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
+        } else {
+          ws.P[g] = acc;
+        }
+        atomicAdd(ws.S + slot, acc);
+      }
+      continue;
+    }
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
 #pragma unroll
@@ -1008,19 +1030,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     }
     const bool cont = s_soff < B0;  // the run started in an earlier round
     if (cont) acc += carry;
-    if (kSec) {
-      unsigned long long excl = __shfl_up_sync(kFull, acc, 1);
-      if (lane == rs) excl = cont ? carry : 0ull;
-      if (g < T) {  // the two checkpoints of a segment are adjacent: one 16-byte store
-        const unsigned long long c0v = excl + acc8;
-        ulonglong2 pr;
-        pr.x = c0v;
-        pr.y = acc;
-        *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
-      }
-    } else if (g < T) {
-      ws.P[g] = acc;
-    }
+    if (g < T) ws.P[g] = acc;
     carry = __shfl_sync(kFull, acc, 31);
   }
   __syncwarp();
@@ -1052,9 +1062,9 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       if (zm != kUnsampled) continue;
       C1 = row_count(E, s_nnz, K1);
     }
-    constexpr uint32_t kCk = kSec ? 2u : 1u;  // checkpoints per segment
+    constexpr uint32_t kCk = kSec ? 2u : 1u;  // chunk sums / checkpoints per segment
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
-    const unsigned long long Spi = nck ? ws.P[c0 + nck - 1u] : 0ull;
+    const unsigned long long Spi = kChunk ? ws.S[slot] : (nck ? ws.P[c0 + nck - 1u] : 0ull);
     const double Sp = (double)Spi * inv_s;  // exact: Spi < 2^48
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
@@ -1076,14 +1086,26 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         // in exact integers against Yf = floor(y 2^s)  (P > y  <=>  P > Yf for integer P)
         const double y = x - M;
         const unsigned long long Yf = (unsigned long long)(y * scl[1]);
-        uint32_t a = c0, b = c0 + nck - 1u;
-        while (a < b) {
-          const uint32_t mid = (a + b) >> 1;
-          if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
+        uint32_t a = c0;
+        unsigned long long base = 0ull;
+        if (kChunk) {  // walk the run's chunk sums: the chunk whose running prefix passes Yf
+          const uint32_t cl = c0 + nck - 1u;
+          while (a < cl) {
+            const unsigned long long q = ws.P[a];
+            if (base + q > Yf) break;
+            base += q;
+            ++a;
+          }
+        } else {  // binary search over the run's prefix checkpoints
+          uint32_t b = c0 + nck - 1u;
+          while (a < b) {
+            const uint32_t mid = (a + b) >> 1;
+            if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
+          }
+          base = (a > c0) ? ws.P[a - 1u] : 0ull;
         }
-        const unsigned long long base = (a > c0) ? ws.P[a - 1u] : 0ull;
         unsigned long long pb = base, pa = base;  // prefixes before / after the candidate
-        if (kSec || kSegW == 8u) {  // one sector (8 entries; zero padding past nnz) from registers
+        if (kChunk) {  // one sector (8 entries; zero padding past nnz) from registers
           uint4 qa, qb;
           ldg256(E + (a - c0) * 8u, qa, qb);
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -1419,6 +1441,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     unsigned char* wb = slots + nsl * sb + warp * d.ws_bytes;
     ws.P = reinterpret_cast<unsigned long long*>(wb);
     ws.q = reinterpret_cast<uint32_t*>(wb + d.ws_bytes - 4u * kQueue);
+    ws.S = reinterpret_cast<unsigned long long*>(wb + d.ws_bytes - 4u * kQueue - 8u * 32u);
   }
   // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
   auto hist_of = [&](uint32_t sl) -> uint32_t* {
@@ -1576,6 +1599,33 @@ __global__ void __launch_bounds__(256) k_wcount(Dev d, Buf cur, Buf nxt) {
   }
   __syncthreads();
   item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
+}
+
+// H7 (world > 1): global packed tail row of tail word t from every rank's word-major tail
+// topics (all-gathered): segment r of word t is tz_all[r * tail_max + off_r[t] .. off_r[t+1]).
+// Block per tail word: shared histogram, ordered compaction (integer: identical on all ranks).
+__global__ void __launch_bounds__(256) k_tail_rebuild(Dev d, Buf nxt, const uint16_t* tz_all, const uint32_t* off,
+                                                      uint32_t world, uint64_t tail_max) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  __shared__ uint32_t s_wsum[32], s_run;
+  const uint32_t t = blockIdx.x, Vt = d.V - d.Vd;
+  uint32_t tot = 0;
+  for (uint32_t r = 0; r < world; ++r) tot += off[(size_t)r * (Vt + 1) + t + 1] - off[(size_t)r * (Vt + 1) + t];
+  if (tot == 0) {  // no token of the word on any rank
+    if (threadIdx.x == 0) nxt.tnnz[t] = 0;
+    return;
+  }
+  for (uint32_t k = threadIdx.x; k < d.Kpad; k += blockDim.x) hist[k] = 0;
+  __syncthreads();
+  for (uint32_t r = 0; r < world; ++r) {
+    const uint32_t o0 = off[(size_t)r * (Vt + 1) + t], o1 = off[(size_t)r * (Vt + 1) + t + 1];
+    const uint16_t* src = tz_all + (size_t)r * tail_max;
+    for (uint32_t i = o0 + threadIdx.x; i < o1; i += blockDim.x) atomicAdd(&hist[src[i]], 1u);
+  }
+  __syncthreads();
+  const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, &s_run, 16u);
+  if (threadIdx.x == 0) nxt.tnnz[t] = nz;
 }
 
 // ---------------------------------------------------------------------------------
@@ -1816,7 +1866,7 @@ constexpr size_t kMaxSmem = 227u * 1024u;
 SamplerLayout sampler_layout(uint32_t K) {
   SamplerLayout L{};
   const uint32_t Kpad = (K + 31) / 32 * 32;
-  L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
+  L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 8u * 32u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it)
   // with >= 2 slots, the most slots first (A/B: 3 slots vs 2 -- PubMed 77.1 -> 76.0 ms,
@@ -1895,6 +1945,7 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   if (nb < 1) return cudaErrorInvalidConfiguration;
   *grid = (uint32_t)(nsm * nb);
   if ((e = raise_smem(dev, (const void*)k_wcount, (int)wcount_smem_bytes(K)))) return e;
+  if ((e = raise_smem(dev, (const void*)k_tail_rebuild, (int)wcount_smem_bytes(K)))) return e;
   if (two_branch_word_major(K) && (e = raise_smem(dev, (const void*)k_tb_item, (int)tb_item_smem_bytes(K))))
     return e;
   if ((e = raise_smem(dev, (const void*)k_doc_block<false>, db))) return e;
@@ -1966,6 +2017,12 @@ void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_
   k_tb_prep<<<d.V, 256, 0, s>>>(d, cur);
   k_tb_draw<<<(d.Dn + 7) / 8, 256, 0, s>>>(d, nxt, iteration);
   if (n_items) k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, nxt, nxt);
+}
+
+void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, const uint32_t* off, uint32_t world,
+                         uint64_t tail_max, cudaStream_t s) {
+  const uint32_t Vt = d.V - d.Vd;
+  if (Vt) k_tail_rebuild<<<Vt, 256, wcount_smem_bytes(d.K), s>>>(d, nxt, tz_all, off, world, tail_max);
 }
 
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {

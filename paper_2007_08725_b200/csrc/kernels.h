@@ -121,6 +121,9 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
 void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
                        cudaStream_t s);
 bool two_branch_word_major(uint32_t K);
+// H7 (world > 1): global tail rows from every rank's all-gathered word-major tail topics
+void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, const uint32_t* off, uint32_t world,
+                         uint64_t tail_max, cudaStream_t s);
 void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s);
 
 // ----- setup / IO kernels -----

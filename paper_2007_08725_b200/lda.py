@@ -46,7 +46,7 @@ class IterStats(C.Structure):
         ("n_tokens", C.c_uint64), ("skip_S", C.c_uint64), ("skip_final", C.c_uint64), ("sampled", C.c_uint64),
         ("active_runs", C.c_uint64), ("drow_words", C.c_uint64), ("d_nnz", C.c_uint64),
         ("model_bytes", C.c_double), ("model_bytes_sample", C.c_double), ("model_bytes_docpass", C.c_double),
-        ("kernel_launches", C.c_uint64), ("exact_redraws", C.c_uint64),
+        ("kernel_launches", C.c_uint64), ("exact_redraws", C.c_uint64), ("exchange_bytes", C.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -495,13 +495,44 @@ def test_set_topics_validates_device_input(ez, tiny):
 
 
 def test_local_group_world_mismatch_rejected(ez, tiny):
-    """A local_group key in use with another world is rejected; the key is reusable after the
-    group's handles are destroyed."""
+    """A local_group key in use with another world is rejected at once; the group then
+    completes with the right world, and the key is reusable once its handles are destroyed
+    (ADVICE r01)."""
+    import threading
+
     w, d = tiny
     n = len(w) // 2
-    a = ez.EzLDA(w[:n], d[:n], TINY["n_docs"], TINY["V"], 16, rank=0, world=2, local_group=777)
+    out = {}
+
+    def rank0():
+        out[0] = ez.EzLDA(w[:n], d[:n], TINY["n_docs"], TINY["V"], 16, rank=0, world=2, local_group=777)
+
+    t = threading.Thread(target=rank0)
+    t.start()
+    import time
+
+    time.sleep(2.0)  # rank 0 registered the key (it now waits for rank 1 in create)
     with pytest.raises(ez.EzLDAError, match="E_INVALID"):
         ez.EzLDA(w[n:], d[n:], TINY["n_docs"], TINY["V"], 16, rank=1, world=3, local_group=777)
-    a.close()
-    b = ez.EzLDA(w, d, TINY["n_docs"], TINY["V"], 16, rank=0, world=1, local_group=777)
+    b = ez.EzLDA(w[n:], d[n:], TINY["n_docs"], TINY["V"], 16, rank=1, world=2, local_group=777, token_base=n)
+    t.join(timeout=120)
+    assert 0 in out
+    out[0].close()
     b.close()
+    # the key is free again: a 3-rank group reuses it
+    hs, errs = {}, []
+
+    def rank_main(r, world=3):
+        try:
+            t0, t1 = r * len(w) // world, (r + 1) * len(w) // world
+            hs[r] = ez.EzLDA(w[t0:t1], d[t0:t1], TINY["n_docs"], TINY["V"], 16, rank=r, world=world,
+                             local_group=777, token_base=t0)
+        except Exception as e:
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(3)]
+    for x in ts:
+        x.start()
+    for x in ts:
+        x.join(timeout=120)
+    assert not errs and len(hs) == 3, errs

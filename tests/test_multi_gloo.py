@@ -84,3 +84,77 @@ def test_two_rank_gloo_equals_single(tmp_path, branches):
     ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED, branches=branches)
     ref.iterate(ITERS)
     assert np.array_equal(np.load(out), ref.topics().astype(np.int64))
+
+
+def worker_hybrid(rank, world, port, out):
+    """The library's H7 protocol on CPU: global word counts decide the dense set
+    (c_v > K); per iteration the dense block [V_d x K] and n_k are all-reduced (sum), and the
+    tail words' topics are all-gathered in word-major order (padded to the largest rank's
+    tail-token count, static per-rank offsets exchanged once) and every rank rebuilds the
+    global tail rows from them.  The per-rank chain is the CPU oracle fed the merged W."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle
+
+    w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
+    L = np.bincount(d, minlength=N_DOCS)
+    bounds = partition_docs(L, world)
+    cum = np.concatenate([[0], np.cumsum(L)])
+    t0, t1 = int(cum[bounds[rank]]), int(cum[bounds[rank + 1]])
+    ws, ds = w[t0:t1], d[t0:t1] - bounds[rank]
+    shard = oracle.OracleLDA(ws, ds, bounds[rank + 1] - bounds[rank], V, K, seed=SAMPLER_SEED, token_base=t0)
+    # create: global counts -> dense set; static per-rank tail layout
+    cnt = torch.from_numpy(np.bincount(ws, minlength=V).astype(np.int64))
+    dist.all_reduce(cnt)
+    dense = cnt.numpy() > K
+    tail_words = np.nonzero(~dense)[0]
+    local_tail_tok = np.nonzero(~dense[ws])[0]
+    local_tail_tok = local_tail_tok[np.argsort(ws[local_tail_tok], kind="stable")]  # word-major
+    n_loc = torch.tensor([len(local_tail_tok)])
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, n_loc)
+    tail_max = int(max(s.item() for s in sizes))
+    for _ in range(ITERS):
+        z = shard.topics()
+        Wl = shard.counts()[1].astype(np.int64)
+        Wd = torch.from_numpy(Wl[dense].copy())
+        nk = torch.from_numpy(Wl.sum(0))
+        dist.all_reduce(Wd)
+        dist.all_reduce(nk)
+        tz = torch.full((tail_max, 2), -1, dtype=torch.int64)  # (word, topic) of each tail token
+        tz[: len(local_tail_tok), 0] = torch.from_numpy(ws[local_tail_tok].astype(np.int64))
+        tz[: len(local_tail_tok), 1] = torch.from_numpy(z[local_tail_tok].astype(np.int64))
+        parts = [torch.zeros_like(tz) for _ in range(world)]
+        dist.all_gather(parts, tz)
+        allt = torch.cat(parts).numpy()
+        allt = allt[allt[:, 0] >= 0]
+        Wg = np.zeros((V, K), np.int64)
+        Wg[dense] = Wd.numpy()
+        np.add.at(Wg, (allt[:, 0], allt[:, 1]), 1)  # the rebuilt global tail rows
+        assert np.array_equal(Wg.sum(0), nk.numpy())
+        assert np.all(Wg[tail_words].sum(1) == cnt.numpy()[tail_words])
+        shard.iterate(1, Wg.astype(np.int32), nk.numpy().astype(np.int32))
+    zt = torch.from_numpy(shard.topics().astype(np.int64))
+    mx = int(max(s for s in [len(w)]))
+    pad = torch.full((mx,), -1, dtype=torch.int64)
+    pad[: len(zt)] = zt
+    allp = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allp, pad)
+    if rank == 0:
+        np.save(out, np.concatenate([p[p >= 0].numpy() for p in allp]))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_hybrid_exchange_equals_single(tmp_path):
+    """Dense-block all-reduce + tail-topic all-gather (the H7 protocol of the library) equals
+    the single chain bit for bit."""
+    from oracle import oracle
+
+    oracle.build()
+    out = str(tmp_path / "z.npy")
+    mp.spawn(worker_hybrid, args=(2, free_port(), out), nprocs=2, join=True)
+    w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
+    ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED)
+    ref.iterate(ITERS)
+    assert np.array_equal(np.load(out), ref.topics().astype(np.int64))
