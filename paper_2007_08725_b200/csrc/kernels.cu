@@ -293,144 +293,160 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
   }
 }
 
-// H1: word-prep, large K.  One THREAD per word: the word's What
-// values are formed on the fly in ascending topic order (dense rows: (W + beta) / den_k;
-// tail rows: the absent-pair value beta / den_k merged with the sorted nonzeros), pass 1
-// keeps the top-4 (value desc, topic asc), pass 2 writes the fixed-point What' row for the
-// sampler and runs the Q' prefix P_v(k) strictly sequentially -- the oracle's order, so
-// QP[k] = alpha P_v(k) and Q' = alpha P_v(K-1) are its values bit for bit.  32 words per
-// warp run their sequential chains side by side (all lanes busy).
-struct WhatCursor {  // What[v][k] for ascending k
-  const int32_t* wd;    // dense row or nullptr
-  const uint32_t* tr;   // tail packed row (topic << 16 | count)
-  uint32_t n, e, nk;    // tail nnz, cursor, next nonzero topic (0xFFFFFFFF: none)
-};
+// H1: word-prep, large K (K > 4096).  One warp per word, the What row in 256-topic chunks
+// staged in shared memory (2 KB per warp, so occupancy does not fall with K).  Pass 1: every
+// chunk filled with What[v][k] = (W[v][k] + beta) / den_k (dense rows; tail rows: the
+// absent-pair value beta / den_k with the sorted nonzeros merged in), per-lane top-4 lists
+// + a 4-round warp tournament (value desc, topic asc).  Pass 2: the chunks refilled, the K1
+// entry zeroed (What', Eq 6), m written by all lanes, and lane 0 runs the Q' prefix P_v(k)
+// strictly sequentially across the chunks -- the oracle's order, so QP[k] = alpha P_v(k) and
+// Q' = alpha P_v(K-1) are its values bit for bit; qfx / ce are written from each finished
+// chunk with the scale 2^t fixed in pass 1 from a (parallel) estimate of Q'.
+constexpr uint32_t kWbWarps = 8;
+constexpr uint32_t kWbChunk = 256;
 
-__device__ __forceinline__ double what_next(const Dev& d, WhatCursor& c, uint32_t k) {
-  if (c.wd) return ((double)c.wd[k] + d.beta) / d.den[k];
-  if (k == c.nk) {
-    const uint32_t p = c.tr[c.e];
-    ++c.e;
-    c.nk = (c.e < c.n) ? (c.tr[c.e] >> 16) : 0xFFFFFFFFu;
-    return ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
-  }
-  return __ldg(d.what0 + k);
-}
-
-__device__ __forceinline__ void what_reset(const Dev& d, const Buf& cur, uint32_t v, WhatCursor& c) {
+// What[v][c0 .. c0 + kWbChunk) into ch (zero past K); tcur: warp-uniform cursor into the
+// word's tail row (entries below c0 were consumed by earlier chunks)
+__device__ __forceinline__ void fill_what_chunk(const Dev& d, const Buf& cur, uint32_t v, uint32_t c0, double* ch,
+                                                uint32_t& tcur) {
+  const uint32_t lane = threadIdx.x & 31u;
   if (v < d.Vd) {
-    c.wd = cur.Wd + (size_t)v * d.K;
-    c.tr = nullptr;
-    c.n = c.e = 0;
-    c.nk = 0xFFFFFFFFu;
+    const int32_t* w = cur.Wd + (size_t)v * d.K;
+    for (uint32_t i = lane; i < kWbChunk; i += 32u) {
+      const uint32_t k = c0 + i;
+      ch[i] = (k < d.K) ? ((double)w[k] + d.beta) / d.den[k] : 0.0;
+    }
   } else {
-    const uint32_t t = v - d.Vd;
-    c.wd = nullptr;
-    c.tr = cur.Wt + d.tofs[t];
-    c.n = cur.tnnz[t];
-    c.e = 0;
-    c.nk = c.n ? (c.tr[0] >> 16) : 0xFFFFFFFFu;
-  }
-}
-
-constexpr uint32_t kWpChunk = 16;  // k_word_prep_t: entries per lane between cooperative row writes
-
-__global__ void __launch_bounds__(128) k_word_prep_t(Dev d, Buf cur) {
-  // pass-2 outputs of the warp's 32 words, staged per 16-entry chunk so that every row is
-  // written with contiguous stores instead of 32 scattered rows per store instruction
-  __shared__ uint32_t s_m[4][32][kWpChunk + 1];
-  __shared__ double s_q[4][32][kWpChunk + 1];
-  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31u, wi = threadIdx.x >> 5;
-  const bool act = v < d.V && d.wtok[v + 1] != d.wtok[v];  // else no token of v in this shard
-  const bool out = act && v < d.Vw;
-  const uint32_t outmask = __ballot_sync(kFull, out);
-  const uint32_t vbase = v - lane;
-  double two_t = 0.0;
-  WhatCursor c;
-  WordRec r;
-  uint32_t K1 = 0xFFFFFFFFu;
-  int sh = 0;
-  if (act) {
-    what_reset(d, cur, v, c);
-    Top4 t;
-    top4_init(t);
-    for (uint32_t k = 0; k < d.K; ++k) top4_insert(t, what_next(d, c, k), k);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool ok = t.v[i] >= 0.0;
-      r.a[i] = ok ? t.v[i] : 0.0;
-      r.K[i] = ok ? (uint16_t)t.k[i] : (uint16_t)0;
-    }
-    K1 = r.K[0];
-    int e = 0;
-    frexp(r.a[1], &e);  // max What' = a2; fixed point m = rint(What' 2^sh), max in [2^31, 2^32)
-    sh = 32 - e;
-    if (out) {
-      WrowPtrs o = wrow_ptrs(d, v);
-      o.sc[0] = ldexp(1.0, -sh);
-      o.sc[1] = ldexp(1.0, sh);
-    }
-    what_reset(d, cur, v, c);
-  }
-  double acc = 0.0;
-  for (uint32_t k0 = 0; k0 < d.Kpad; k0 += kWpChunk) {  // warp-uniform trip count (Kpad % 32 == 0)
-#pragma unroll 4
-    for (uint32_t i = 0; i < kWpChunk; ++i) {
-      const uint32_t k = k0 + i;
-      double w = (act && k < d.K) ? what_next(d, c, k) : 0.0;
-      if (k == K1) w = 0.0;  // What' (Eq 6): the maximum entry set to 0
-      acc = acc + w;
-      if (k == d.K - 1u) r.Qp = d.alpha * acc;
-      s_m[wi][lane][i] = __double2uint_rn(fmin(ldexp(w, sh), 4294967295.0));
-      s_q[wi][lane][i] = d.alpha * acc;
+    for (uint32_t i = lane; i < kWbChunk; i += 32u) {
+      const uint32_t k = c0 + i;
+      ch[i] = (k < d.K) ? __ldg(d.what0 + k) : 0.0;
     }
     __syncwarp();
-    for (uint32_t x = lane; x < 32u * kWpChunk; x += 32u) {
-      const uint32_t src = x / kWpChunk, kk = x % kWpChunk;
-      if ((outmask >> src) & 1u) {
-        WrowPtrs o = wrow_ptrs(d, vbase + src);
-        o.m[k0 + kk] = s_m[wi][src][kk];
-        o.qp[k0 + kk] = s_q[wi][src][kk];
+    const uint32_t t = v - d.Vd;
+    const uint32_t* tr = cur.Wt + d.tofs[t];
+    const uint32_t n = cur.tnnz[t];
+    while (tcur < n) {  // the row's entries with topic in [c0, c0 + kWbChunk) (sorted by topic)
+      const uint32_t e = tcur + lane;
+      const uint32_t p = (e < n) ? tr[e] : 0u;
+      const uint32_t k = p >> 16;
+      const bool in = e < n && k < c0 + kWbChunk;
+      if (in) ch[k - c0] = ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
+      const uint32_t cnt = __popc(__ballot_sync(kFull, in));
+      tcur += cnt;
+      if (cnt < 32u) break;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur) {
+  __shared__ double s_ch[kWbWarps][kWbChunk];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t v = blockIdx.x * kWbWarps + warp;
+  if (v >= d.V || d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard (warp-uniform)
+  double* ch = s_ch[warp];
+  // ---- pass 1: top-4 (value desc, topic asc) and an estimate of sum_k What
+  Top4 t;
+  top4_init(t);
+  double tot = 0.0;
+  uint32_t tcur = 0;
+  for (uint32_t c0 = 0; c0 < d.K; c0 += kWbChunk) {
+    fill_what_chunk(d, cur, v, c0, ch, tcur);
+    for (uint32_t i = lane; i < kWbChunk && c0 + i < d.K; i += 32u) {
+      const double x = ch[i];
+      top4_insert(t, x, c0 + i);
+      tot += x;
+    }
+    __syncwarp();
+  }
+  WordRec r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double bv = t.v[0];
+    uint32_t bk = t.k[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, bv, o);
+      const uint32_t ok = __shfl_xor_sync(kFull, bk, o);
+      if (better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
+    }
+    if (t.k[0] == bk) {  // the owner pops its head
+      t.v[0] = t.v[1]; t.k[0] = t.k[1];
+      t.v[1] = t.v[2]; t.k[1] = t.k[2];
+      t.v[2] = t.v[3]; t.k[2] = t.k[3];
+      t.v[3] = -1.0; t.k[3] = 0xFFFFFFFFu;
+    }
+    const bool ok = bv >= 0.0;
+    r.a[i] = ok ? bv : 0.0;
+    r.K[i] = ok ? (uint16_t)bk : (uint16_t)0;
+  }
+  tot = warp_sum(tot);
+  const uint32_t K1 = r.K[0];
+  // scales: m = rint(What' 2^sh) with max What' = a2 in [2^31, 2^32) 2^-sh; qfx = rint(QP 2^t)
+  // with 2^t from the estimate of Q' (1 + 2^-30 covers its rounding: no entry saturates)
+  int e = 0;
+  frexp(r.a[1], &e);
+  const int sh = 32 - e;
+  int et = 0;
+  frexp(d.alpha * (tot - r.a[0]) * (1.0 + 0x1p-30), &et);
+  const double two_t = ldexp(1.0, 32 - et);
+  const bool out = v < d.Vw;
+  WrowPtrs o = wrow_ptrs(d, v);
+  // ---- pass 2: What' chunks -> m; lane 0's sequential Q' prefix -> QP, qfx, ce
+  double acc = 0.0;
+  tcur = 0;
+  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += kWbChunk) {
+    fill_what_chunk(d, cur, v, c0, ch, tcur);
+    if (lane == 0 && K1 >= c0 && K1 < c0 + kWbChunk) ch[K1 - c0] = 0.0;  // What' (Eq 6)
+    __syncwarp();
+    const uint32_t n = min(kWbChunk, d.Kpad - c0);
+    if (out)
+      for (uint32_t i = lane; i < n; i += 32u) o.m[c0 + i] = __double2uint_rn(fmin(ldexp(ch[i], sh), 4294967295.0));
+    __syncwarp();
+    if (lane == 0) {  // strictly sequential (ascending k); 8 entries loaded ahead of the adds
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = ch[i];
+      for (uint32_t i0 = 0; i0 < n; i0 += 8u) {
+        double xn[8];
+        const uint32_t in = (i0 + 8u < n) ? i0 + 8u : i0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xn[i] = ch[in + i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc = acc + x[i];
+          ch[i0 + i] = d.alpha * acc;
+          if (c0 + i0 + i == d.K - 1u) r.Qp = d.alpha * acc;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = xn[i];
+      }
+    }
+    __syncwarp();
+    if (out) {
+      for (uint32_t i = lane; i < n; i += 32u) {
+        const double q = ch[i];
+        o.qp[c0 + i] = q;
+        o.qfx[c0 + i] = __double2uint_rn(fmin(q * two_t, 4294967295.0));
+      }
+      for (uint32_t i = 31u + 32u * lane; i < n; i += 32u * 32u) {  // chunk ends of this chunk
+        const uint32_t c = (c0 + i) >> 5;
+        o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(ch[i] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
       }
     }
     __syncwarp();
   }
-  if (act) {
-    d.rec[v] = r;
-    if (out) {
-      WrowPtrs o = wrow_ptrs(d, v);
-      int e = 0;
-      frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
-      two_t = ldexp(1.0, 32 - e);
-      o.sc[2] = ldexp(1.0, e - 32);
+  r.Qp = __shfl_sync(kFull, r.Qp, 0);
+  if (out) {
+    for (uint32_t c = d.nch + lane; c < ce_words(d.Kpad); c += 32u) o.ce[c] = 0xFFFFFFFFu;
+    if (lane == 0) {
+      o.sc[0] = ldexp(1.0, -sh);
+      o.sc[1] = ldexp(1.0, sh);
+      o.sc[2] = 1.0 / two_t;
       o.sc[3] = two_t;
     }
   }
-  // qfx rows of the warp's words, converted cooperatively (coalesced along k)
-  __syncwarp();
-  uint32_t pend = __ballot_sync(kFull, out);
-  while (pend) {
-    const uint32_t src = __ffs(pend) - 1u;
-    pend &= pend - 1u;
-    const uint32_t vw = __shfl_sync(kFull, v, src);
-    const double tt = __shfl_sync(kFull, two_t, src);
-    WrowPtrs o = wrow_ptrs(d, vw);
-    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane (qp and qfx
-      double x[8];                                      // share the buffer: no implicit reordering)
-#pragma unroll
-      for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t k = k0 + 32u * i + lane;
-        x[i] = (k < d.Kpad) ? o.qp[k] : 0.0;
-      }
-#pragma unroll
-      for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t k = k0 + 32u * i + lane;
-        if (k < d.Kpad) o.qfx[k] = __double2uint_rn(fmin(x[i] * tt, 4294967295.0));
-      }
-    }
-    for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)
-      o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(o.qp[32u * c + 31u] * tt, 4294967295.0)) : 0xFFFFFFFFu;
-  }
+  if (lane == 0) d.rec[v] = r;
 }
 
 // ---------------------------------------------------------------------------------
@@ -760,9 +776,8 @@ struct RunCounters {
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | run sums | queue
-  unsigned long long* P;  // fixed-point chunk sums / prefix checkpoints of the batch's runs (sample_batch)
-  unsigned long long* S;  // [32] fixed-point S' of each run of the batch (8/16-entry segments)
+struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | queue
+  unsigned long long* P;  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
   uint32_t* q;            // queue of flagged runs
 };
 
@@ -801,6 +816,13 @@ __device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc,
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
+               "l"(src), "r"(bytes), "r"(mbar_s)
+               : "memory");
+}
+
+// bulk copy completing on an mbarrier whose expect_tx was already posted
+__device__ __forceinline__ void bulk_copy_tx(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
                "l"(src), "r"(bytes), "r"(mbar_s)
                : "memory");
@@ -908,9 +930,10 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 // of the fast path (x vs M, x vs M + S', the S' and Q' descents) is taken only if it holds
 // with a margin bounding that error (2 L_d 2^-s + 4e-15 Z); otherwise the token is redrawn
 // by exact_draw.  Either way the topic equals the oracle's fp64 decision.
-template <uint32_t kSegW, bool kQG>
+template <uint32_t kSegW, uint32_t kSub, bool kQG>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
-                                                 uint32_t v, uint32_t row_s, const uint32_t* qfx, const double* scl,
+                                                 uint32_t v, uint32_t row_s, const uint32_t* qfx, const uint32_t* ce,
+                                                 const double* scl,
                                                  const double* const* qpp, uint32_t* hist, WarpScratch& ws,
                                                  uint32_t qn, uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -935,7 +958,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t y = __shfl_up_sync(kFull, sincl, o);
     if (lane >= (uint32_t)o) sincl += y;
   }
-  constexpr uint32_t kCap = (kSegW == 8u) ? 2u * kSegCap : kSegCap;  // segments per batch
+  // checkpoints per segment: one per kSub-entry chunk (kSub = 8: one per 32-byte sector, so a
+  // descent walks one sector from registers; kSub = kSegW: one per segment)
+  constexpr uint32_t kCk = kSegW / kSub;
+  constexpr uint32_t kCap = (kSub == 8u ? 2u * kSegCap : kSegCap) / kCk;  // segments per batch
   const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));  // >= 1
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
   const uint32_t soff = sincl - nseg;
@@ -966,20 +992,11 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t j = __shfl_sync(kFull, j0, slot) + (lane - __shfl_sync(kFull, tofs, slot));
     if (lane < ntb) zpre = nxt.z[j];
   }
-  // ---- B: lane per segment (kSegW entries, 16 = two 32-byte sectors); consecutive lanes
-  //      read consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the
-  //      word's fixed-point What' row).
-  //      kSegW <= 16 (kChunk): every lane stores the sums of its 8-entry chunks (sectors), P[c],
-  //      and adds its segment total to the run's S' (shared 64-bit atomic) -- no scan: the
-  //      rare S'-branch descent walks the chunk sums of its run (phase D).
-  //      kSegW >= 32: a segmented warp scan (+ carry across rounds) turns segment sums into
-  //      run prefixes P[g] = P(end of g); S' = the run's last one (binary-searched in D).
-  constexpr bool kChunk = kSegW <= 16u;
-  constexpr bool kSec = kSegW == 16u;
-  if (kChunk) {
-    if (lane < nb) ws.S[lane] = 0ull;
-    __syncwarp();
-  }
+  // ---- B: lane per segment (kSegW entries = kSegW / 8 sectors); consecutive lanes read
+  //      consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the word's
+  //      fixed-point What' row), combined by a segmented warp scan (+ carry across rounds).
+  //      Checkpoints: P[kCk g + i] = P(before g) + (chunks 0..i of g); the last one is
+  //      P(end of g), and S' = the run's last checkpoint.
   unsigned long long carry = 0ull;
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
     const uint32_t g = B0 + lane;
@@ -989,12 +1006,26 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
     const uint32_t e0 = (g - s_soff) * kSegW;
     const uint32_t* p = d.D + s_ebase + e0;
-    unsigned long long acc = 0ull, acc8 = 0ull;
+    unsigned long long acc = 0ull;
+    unsigned long long part[kCk > 1 ? kCk - 1 : 1];  // running sums after chunks 0 .. kCk-2
     if (g < T) {
       if (kSegW == 8u) {  // one sector per lane and round (fewer live registers)
         uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa;
         if (e0 < s_nnz) ldg256(p, qa, qb);
         acc = sector_mac(acc, qa, qb, row_s);
+      } else if (kSegW == 32u && kSub == 8u) {  // four sectors in flight, then accumulated in order
+        uint4 q[8];
+#pragma unroll
+        for (uint32_t b = 0; b < 4u; ++b) {
+          q[2 * b] = make_uint4(0u, 0u, 0u, 0u);
+          q[2 * b + 1] = q[2 * b];
+          if (e0 + 8u * b < s_nnz) ldg256(p + 8u * b, q[2 * b], q[2 * b + 1]);
+        }
+#pragma unroll
+        for (uint32_t b = 0; b < 4u; ++b) {
+          acc = sector_mac(acc, q[2 * b], q[2 * b + 1], row_s);
+          if (b < 3u) part[b < kCk - 1 ? b : 0] = acc;
+        }
       } else {
 #pragma unroll
         for (uint32_t b = 0; b < kSegW; b += 16u) {
@@ -1002,25 +1033,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
           if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
           acc = sector_mac(acc, qa, qb, row_s);
-          if (kSec) acc8 = acc;
+          if (kCk == 2u) part[0] = acc;
           acc = sector_mac(acc, qc, qd, row_s);
         }
       }
     }
-    if (kChunk) {
-      if (g < T) {
-        if (kSec) {  // the two sector sums of the segment are adjacent: one 16-byte store
-          ulonglong2 pr;
-          pr.x = acc8;
-          pr.y = acc - acc8;
-          *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
-        } else {
-          ws.P[g] = acc;
-        }
-        atomicAdd(ws.S + slot, acc);
-      }
-      continue;
-    }
+    const unsigned long long tot = acc;
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
 #pragma unroll
@@ -1028,9 +1046,28 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       const unsigned long long y = __shfl_up_sync(kFull, acc, o);
       if (lane >= rs + (uint32_t)o) acc += y;
     }
-    const bool cont = s_soff < B0;  // the run started in an earlier round
-    if (cont) acc += carry;
-    if (g < T) ws.P[g] = acc;
+    if (s_soff < B0) acc += carry;  // the run started in an earlier round
+    if (g < T) {
+      if (kCk == 1u) {
+        ws.P[g] = acc;
+      } else {
+        const unsigned long long excl = acc - tot;  // prefix before segment g
+        if (kCk == 2u) {  // the two checkpoints of a segment are adjacent: one 16-byte store
+          ulonglong2 pr;
+          pr.x = excl + part[0];
+          pr.y = acc;
+          *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
+        } else {
+          ulonglong2 pr0, pr1;
+          pr0.x = excl + part[0];
+          pr0.y = excl + part[kCk > 2 ? 1 : 0];
+          pr1.x = excl + part[kCk > 3 ? 2 : 0];
+          pr1.y = acc;
+          *reinterpret_cast<ulonglong2*>(ws.P + kCk * g) = pr0;
+          *reinterpret_cast<ulonglong2*>(ws.P + kCk * g + 2u) = pr1;
+        }
+      }
+    }
     carry = __shfl_sync(kFull, acc, 31);
   }
   __syncwarp();
@@ -1062,9 +1099,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       if (zm != kUnsampled) continue;
       C1 = row_count(E, s_nnz, K1);
     }
-    constexpr uint32_t kCk = kSec ? 2u : 1u;  // chunk sums / checkpoints per segment
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
-    const unsigned long long Spi = kChunk ? ws.S[slot] : (nck ? ws.P[c0 + nck - 1u] : 0ull);
+    const unsigned long long Spi = nck ? ws.P[c0 + nck - 1u] : 0ull;
     const double Sp = (double)Spi * inv_s;  // exact: Spi < 2^48
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
@@ -1086,26 +1122,14 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         // in exact integers against Yf = floor(y 2^s)  (P > y  <=>  P > Yf for integer P)
         const double y = x - M;
         const unsigned long long Yf = (unsigned long long)(y * scl[1]);
-        uint32_t a = c0;
-        unsigned long long base = 0ull;
-        if (kChunk) {  // walk the run's chunk sums: the chunk whose running prefix passes Yf
-          const uint32_t cl = c0 + nck - 1u;
-          while (a < cl) {
-            const unsigned long long q = ws.P[a];
-            if (base + q > Yf) break;
-            base += q;
-            ++a;
-          }
-        } else {  // binary search over the run's prefix checkpoints
-          uint32_t b = c0 + nck - 1u;
-          while (a < b) {
-            const uint32_t mid = (a + b) >> 1;
-            if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
-          }
-          base = (a > c0) ? ws.P[a - 1u] : 0ull;
+        uint32_t a = c0, b = c0 + nck - 1u;
+        while (a < b) {
+          const uint32_t mid = (a + b) >> 1;
+          if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
         }
+        const unsigned long long base = (a > c0) ? ws.P[a - 1u] : 0ull;
         unsigned long long pb = base, pa = base;  // prefixes before / after the candidate
-        if (kChunk) {  // one sector (8 entries; zero padding past nnz) from registers
+        if (kSub == 8u) {  // one sector (8 entries; zero padding past nnz) from registers
           uint4 qa, qb;
           ldg256(E + (a - c0) * 8u, qa, qb);
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
@@ -1120,8 +1144,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             }
           }
         } else {
-          const uint32_t e0 = (a - c0) * kSegW;
-          const uint32_t e1 = min(e0 + kSegW, s_nnz);
+          const uint32_t e0 = (a - c0) * kSub;
+          const uint32_t e1 = min(e0 + kSub, s_nnz);
           for (uint32_t e = e0; e < e1; ++e) {
             const uint32_t w = __ldg(E + e);
             const unsigned long long q = entry_mac(w, row_s, pa);
@@ -1146,9 +1170,9 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           const uint32_t Yq = (uint32_t)fmin(y * scl[3], 4294967295.0);  // past the end: uncertified
           uint32_t a = 0, b = d.Kpad - 1u;
           // the table is in the slot (shared memory) or, for large K (kQG), in HBM
+          // (chunk ends ce in the slot either way: the HBM search touches one 128-byte line)
           auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldg(qfx + i) : qfx[i]; };
-          if (!kQG) {  // first the 32-topic chunk from the contiguous chunk ends
-            const uint32_t* ce = qfx + d.Kpad;
+          {  // first the 32-topic chunk from the contiguous chunk ends
             uint32_t ca = 0, cb = d.nch - 1u;
             while (ca < cb) {
               const uint32_t mid = (ca + cb) >> 1;
@@ -1227,14 +1251,15 @@ __device__ __forceinline__ void st_release_s(uint32_t* p, uint32_t v) {
 // per-slot dynamic shared memory: m u32 [Kpad] | qfx u32 [Kpad] | scales f64 [4] (one bulk
 // copy of the word's wrow record head) | hist u32 [Kpad] when it fits (else in HBM scratch)
 __host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad, uint32_t qfx_global) {
-  return qfx_global ? 4u * Kpad + 32u : 8u * Kpad + 32u + 4u * ce_words(Kpad);  // m | scales [| qfx | ce]
+  // m | scales | ce (qfx searched in HBM), or m | scales | qfx | ce
+  return qfx_global ? 4u * Kpad + 32u + 4u * ce_words(Kpad) : 8u * Kpad + 32u + 4u * ce_words(Kpad);
 }
 
 // Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
 // fixed-point What' row, the sequential Q' prefix (the same expressions and order as
 // k_word_prep) into the slot's HBM scratch QP, its fixed-point copy and the scales.
 __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, uint32_t* m,
-                                    uint32_t* qfx, double* sc, double* QP) {
+                                    uint32_t* qfx, uint32_t* ce, double* sc, double* QP) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
   for (uint32_t k0 = lane; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane
@@ -1280,8 +1305,8 @@ __device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, co
   const double two_t = ldexp(1.0, 32 - et);
   __syncwarp();
   for (uint32_t k = lane; k < d.Kpad; k += 32u) qfx[k] = __double2uint_rn(fmin(QP[k] * two_t, 4294967295.0));
-  for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)  // chunk ends right after qfx
-    qfx[d.Kpad + c] = (c < d.nch) ? __double2uint_rn(fmin(QP[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
+  for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)  // chunk ends (in the slot)
+    ce[c] = (c < d.nch) ? __double2uint_rn(fmin(QP[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
   if (lane == 0) {
     sc[0] = ldexp(1.0, -sh);
     sc[1] = ldexp(1.0, sh);
@@ -1325,8 +1350,15 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
       const WrowPtrs o = wrow_ptrs(d, v);
       c.qp = o.qp;
       c.qfx = d.qfx_global ? o.qfx : mrow + d.Kpad + 8u;
-      bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs,
-               slot_head_bytes(d.Kpad, d.qfx_global), mbar_s);
+      if (!d.qfx_global) {  // m | scales | qfx | ce: one contiguous bulk copy
+        bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs,
+                 slot_head_bytes(d.Kpad, 0u), mbar_s);
+      } else {  // m | scales, then the chunk ends ce (the qfx table itself stays in HBM)
+        const uint32_t b1 = 4u * d.Kpad + 32u, b2 = 4u * ce_words(d.Kpad);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(b1 + b2) : "memory");
+        bulk_copy_tx((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, b1, mbar_s);
+        bulk_copy_tx((uint32_t)__cvta_generic_to_shared(mrow) + b1, o.ce, b2, mbar_s);
+      }
     }
   } else {
     uint32_t* qfx = d.qfx_global ? reinterpret_cast<uint32_t*>(qp_scratch + d.Kpad) : mrow + d.Kpad + 8u;
@@ -1335,7 +1367,8 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
       c.qfx = qfx;
     }
     __syncwarp();
-    stage_tail_row_warp(d, cur, v, c.rec, mrow, qfx, reinterpret_cast<double*>(mrow + d.Kpad), qp_scratch);
+    uint32_t* ce = d.qfx_global ? mrow + d.Kpad + 8u : qfx + d.Kpad;
+    stage_tail_row_warp(d, cur, v, c.rec, mrow, qfx, ce, reinterpret_cast<double*>(mrow + d.Kpad), qp_scratch);
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
   }
   __syncwarp();
@@ -1427,7 +1460,7 @@ __host__ __device__ __forceinline__ uint32_t sampler_ctl_bytes() {
 
 // one kernel per (S' segment width, Q' table placement): each gets the register allocation
 // of its own path only
-template <uint32_t kSegW, bool kQG>
+template <uint32_t kSegW, uint32_t kSub, bool kQG>
 __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter,
                                                                   uint32_t n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1441,7 +1474,6 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     unsigned char* wb = slots + nsl * sb + warp * d.ws_bytes;
     ws.P = reinterpret_cast<unsigned long long*>(wb);
     ws.q = reinterpret_cast<uint32_t*>(wb + d.ws_bytes - 4u * kQueue);
-    ws.S = reinterpret_cast<unsigned long long*>(wb + d.ws_bytes - 4u * kQueue - 8u * 32u);
   }
   // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
   auto hist_of = [&](uint32_t sl) -> uint32_t* {
@@ -1482,6 +1514,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
     // fixed-point Q' table: in the slot right after the scales, or in HBM (kQG, large K)
     const uint32_t* qfx = kQG ? c.qfx : reinterpret_cast<const uint32_t*>(slots + sl * sb + 4u * d.Kpad + 32u);
+    const uint32_t* ce = kQG ? reinterpret_cast<const uint32_t*>(slots + sl * sb + 4u * d.Kpad + 32u) : qfx + d.Kpad;
     const double* scl = reinterpret_cast<const double*>(slots + sl * sb + 4u * d.Kpad);
     uint32_t* hist = hist_of(sl);
     const WordRec rec = c.rec;
@@ -1526,7 +1559,8 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
-      const uint32_t nb = sample_batch<kSegW, kQG>(d, cur, nxt, rec, v, row_s, qfx, scl, &c.qp, hist, ws, qn, iter, rc);
+      const uint32_t nb = sample_batch<kSegW, kSub, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, &c.qp, hist, ws, qn,
+                                                         iter, rc);
 
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
@@ -1854,9 +1888,26 @@ uint32_t wrow_stride(uint32_t K) {  // m | scales | qfx | ce | QP (doubles)
 #ifndef EZLDA_SEG_MIN
 #define EZLDA_SEG_MIN 16
 #endif
-uint32_t seg_width(uint32_t K) {  // entries per S' segment: a power of two >= EZLDA_SEG_MIN, K <= kSegCap segw
+#ifndef EZLDA_SEG_QUAD
+#define EZLDA_SEG_QUAD 0  // 1: 32-entry segments with a checkpoint per sector for K <= 4096
+#endif
+// S' segment layout of K: entries per segment (a power of two >= EZLDA_SEG_MIN with
+// K <= segments-per-batch x width, so one run always fits a batch) and entries per checkpoint
+// chunk (8 = one per 32-byte sector up to 16-entry segments, or with EZLDA_SEG_QUAD)
+void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub) {
+  if (EZLDA_SEG_QUAD && K <= (2u * kSegCap / 4u) * 32u) {
+    *segw = 32u;
+    *sub = 8u;
+    return;
+  }
   uint32_t w = EZLDA_SEG_MIN;
   while (w * (w == 8u ? 2u * kSegCap : kSegCap) < K) w <<= 1;
+  *segw = w;
+  *sub = w <= 16u ? 8u : w;
+}
+uint32_t seg_width(uint32_t K) {
+  uint32_t w, sb;
+  seg_config(K, &w, &sb);
   return w;
 }
 constexpr size_t kMaxSmem = 227u * 1024u;
@@ -1866,7 +1917,9 @@ constexpr size_t kMaxSmem = 227u * 1024u;
 SamplerLayout sampler_layout(uint32_t K) {
   SamplerLayout L{};
   const uint32_t Kpad = (K + 31) / 32 * 32;
-  L.ws_bytes = (seg_width(K) <= 16u ? 2u * kSegCap : kSegCap) * 8u + 8u * 32u + 4u * kQueue;
+  uint32_t segw, sub;
+  seg_config(K, &segw, &sub);
+  L.ws_bytes = (sub == 8u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it)
   // with >= 2 slots, the most slots first (A/B: 3 slots vs 2 -- PubMed 77.1 -> 76.0 ms,
@@ -1904,12 +1957,14 @@ bool two_branch_word_major(uint32_t K) { return tb_item_smem_bytes(K) <= 200u * 
 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
-static const void* sampler_kernel(uint32_t segw, uint32_t qg) {
+static const void* sampler_kernel(uint32_t segw, uint32_t sub, uint32_t qg) {
   switch (segw) {  // K <= 16384: segment widths 8 .. 64
-    case 8u: return qg ? (const void*)k_sampler<8u, true> : (const void*)k_sampler<8u, false>;
-    case 16u: return qg ? (const void*)k_sampler<16u, true> : (const void*)k_sampler<16u, false>;
-    case 32u: return qg ? (const void*)k_sampler<32u, true> : (const void*)k_sampler<32u, false>;
-    default: return qg ? (const void*)k_sampler<64u, true> : (const void*)k_sampler<64u, false>;
+    case 8u: return qg ? (const void*)k_sampler<8u, 8u, true> : (const void*)k_sampler<8u, 8u, false>;
+    case 16u: return qg ? (const void*)k_sampler<16u, 8u, true> : (const void*)k_sampler<16u, 8u, false>;
+    case 32u:
+      if (sub == 8u) return qg ? (const void*)k_sampler<32u, 8u, true> : (const void*)k_sampler<32u, 8u, false>;
+      return qg ? (const void*)k_sampler<32u, 32u, true> : (const void*)k_sampler<32u, 32u, false>;
+    default: return qg ? (const void*)k_sampler<64u, 64u, true> : (const void*)k_sampler<64u, 64u, false>;
   }
 }
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
@@ -1938,7 +1993,9 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   if (K <= kWpSmallK && (e = raise_smem(dev, (const void*)k_word_prep_w, (int)word_prep_smem_bytes(K)))) return e;
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if ((e = raise_smem(dev, (const void*)k_llpt, (int)llpt_smem_bytes(K)))) return e;
-  const void* ks = sampler_kernel(seg_width(K), sampler_layout(K).qfx_global);
+  uint32_t segw, sub;
+  seg_config(K, &segw, &sub);
+  const void* ks = sampler_kernel(segw, sub, sampler_layout(K).qfx_global);
   if ((e = raise_smem(dev, ks, sp))) return e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks, kSampWarpsP * 32, (size_t)sp))) return e;
@@ -1966,7 +2023,7 @@ void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s) {
   if (d.K <= kWpSmallK) {
     k_word_prep_w<<<(d.V + kWpWarps - 1) / kWpWarps, kWpWarps * 32, word_prep_smem_bytes(d.K), s>>>(d, cur);
   } else {
-    k_word_prep_t<<<(d.V + 127) / 128, 128, 0, s>>>(d, cur);
+    k_word_prep_big<<<(d.V + kWbWarps - 1) / kWbWarps, kWbWarps * 32, 0, s>>>(d, cur);
   }
 }
 
@@ -2001,7 +2058,7 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
     k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
     {
-      const void* ks = sampler_kernel(d.segw, d.qfx_global);
+      const void* ks = sampler_kernel(d.segw, d.segsub, d.qfx_global);
       const uint32_t grid = std::min<uint32_t>(n_items, d.sampler_grid);
       void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
       cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);
