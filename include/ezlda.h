@@ -35,8 +35,10 @@
  *     and the stream given in the options (or one it creates).
  *   - Threading: one handle per host thread; calls on a handle are serialised.
  *   - Limits (16+16-bit packing): K <= 65535, doc length <= 65535,
- *     tokens per shard < 2^31 (the setup sorts index tokens with int).  This build additionally requires K <= 16384 (the
- *     packed D entries hold the topic in 14 bits; NEXT-2 lifts it).
+ *     tokens per shard < 2^31 (the setup sorts index tokens with int).  K is further
+ *     limited by the sampler's shared-memory slot, which holds the word's fixed-point What'
+ *     row (4 K bytes): K <= ~47,000 on B200 (K = 32768, the paper's headline, works);
+ *     a larger K returns EZLDA_E_RANGE.
  */
 #ifndef EZLDA_H
 #define EZLDA_H

@@ -273,6 +273,7 @@ struct ezlda {
   uint32_t sum_n = 0;
   double* llpt_partial = nullptr;
   double* llpt_out = nullptr;
+  double* llpt_scratch = nullptr;  // large K: per-block fp64 rows of the LLPT kernel (lazily allocated)
   ncclComm_t comm = nullptr;
   ezlda_status sticky = EZLDA_OK;
   std::string err;
@@ -515,6 +516,7 @@ void fill_dev(ezlda* h) {
   d.Vd = h->Vd;
   d.rs = ezl::wrow_stride(h->K);
   ezl::seg_config(h->K, &d.segw, &d.segsub);
+  d.dt = ezl::d_shift(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
   d.c1_cap = (h->debug_flags & EZLDA_DEBUG_C1_LOOKUP) ? 0u : 0x7FFFu;
   {
@@ -881,13 +883,13 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
-  // fixed-point What' | QP rows for every word when they fit in a quarter of the free device
-  // memory, at most 32 GiB (the sampler then stages every item with one bulk copy), else for
+  // fixed-point What' | QP rows for every word when they fit in half of the free device
+  // memory, at most 64 GiB (the sampler then stages every item with one bulk copy), else for
   // the dense words only (tail rows staged by a warp)
   {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
-    const uint64_t budget = std::min<uint64_t>(32ull << 30, fr / 4);
+    const uint64_t budget = std::min<uint64_t>(64ull << 30, fr / 2);
     d.Vw = ((uint64_t)h->V * d.rs * 8ull <= budget) ? h->V : h->Vd;
     if (o.debug_flags & EZLDA_DEBUG_NO_TAIL_ROWS) d.Vw = h->Vd;  // tail rows staged by a sampler warp
     if (h->branches == 2) d.Vw = 0;  // the two-branch mode does not use the three-branch records
@@ -1035,8 +1037,8 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   if (n_tokens == 0 || K == 0 || V == 0 || n_docs == 0) return bad(EZLDA_E_INVALID, "n_tokens, K, V and n_docs must be > 0");
   if (!(alpha > 0.0) || !(beta > 0.0)) return bad(EZLDA_E_INVALID, "alpha and beta must be > 0");
   if (K > 65535) return bad(EZLDA_E_RANGE, "K > 65535 (16-bit topic packing, P:753)");
-  if (K > 16384 || ezl::sampler_slots(K) == 0)
-    return bad(EZLDA_E_RANGE, "K > 16384 not supported by this build (14-bit topic field of the packed D entries)");
+  if (ezl::sampler_slots(K) == 0)
+    return bad(EZLDA_E_RANGE, "K too large for the sampler's shared-memory slot (fixed-point What' row of 4 K bytes)");
   // the setup sorts and scans (CUB) index the shard's tokens with int
   if (n_tokens >= (1ull << 31)) return bad(EZLDA_E_RANGE, "n_tokens >= 2^31 per shard");
   ezlda_options o{};
@@ -1246,7 +1248,7 @@ ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W
         const uint32_t p = Dh[base + ezl::kDHdr + e];
         if (fill) {
           if (nnz >= D->nnz) return h->fail(EZLDA_E_INVALID, "D csr capacity too small");
-          D->col[nnz] = (uint16_t)ezl::d_topic(p);
+          D->col[nnz] = (uint16_t)ezl::d_topic(p, h->dev.dt);
           D->val[nnz] = (int32_t)(p & 0xFFFFu);
         }
         ++nnz;
@@ -1293,7 +1295,11 @@ ezlda_status ezlda_loglik(ezlda* h, double* llpt) {
   if (st) return st;
   Buf& b = h->buf[h->cur];
   ezl::launch_den(h->dev, b, h->stream);
-  ezl::launch_llpt(h->dev, b, h->n_items, h->llpt_partial, h->llpt_out, h->stream);
+  if (!h->llpt_scratch && ezl::llpt_smem_bytes(h->K) > 96u * 1024u) {
+    h->llpt_scratch = h->alloc<double>(ezl::llpt_scratch_doubles(h->K));
+    if (!h->llpt_scratch) return h->fail(EZLDA_E_NOMEM, "LLPT row scratch");
+  }
+  ezl::launch_llpt(h->dev, b, h->n_items, h->llpt_partial, h->llpt_out, h->llpt_scratch, h->stream);
   EZ_CUDA(h, cudaGetLastError());
   if ((st = allreduce(h, h->llpt_out, 1, ncclFloat64))) return st;
   double sum = 0;

@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       uint32_t pos = nnz + incl - cnt;
       for (uint32_t m = b; m; m &= m - 1u) {
         const uint32_t k = wi * 32u + (__ffs(m) - 1u);
-        Drow[pos++] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu);
+        Drow[pos++] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu, d.dt);
       }
       for (uint32_t m = b; m; m &= m - 1u) hist[(wi * 32u + (__ffs(m) - 1u)) >> 1] = 0u;
       if (b) bmp[wi] = 0u;
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(kDocWarps * 32) k_doc_warp(Dev d, Buf cur, Buf
     const uint32_t s1 = (p + 1 < nnz) ? (uint32_t)ust[p + 1] : L;
     const uint32_t cnt = s1 - s0;
     ucnt[p] = (uint16_t)cnt;
-    Drow[kDHdr + p] = d_entry(ukey[p], cnt);
+    Drow[kDHdr + p] = d_entry(ukey[p], cnt, d.dt);
   }
   for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[kDHdr + p] = 0u;  // pad to 8
   if (lane == 0) {
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
   for (uint32_t i = tid; i < L; i += nt) atomicAdd(&hist[cur.z[j0 + i]], 1u);
   __syncthreads();
   uint32_t* Drow = d.D + dbase;
-  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run, kDT);
+  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run, d.dt);
   for (uint32_t p = nnz + tid; p < ((nnz + 7u) & ~7u); p += nt) Drow[kDHdr + p] = 0u;  // pad to 8
   if (tid == 0) {
     Drow[0] = (L << 16) | nnz;
@@ -797,20 +797,24 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 // acc + D[d][k] m_v[k] for one packed entry (topic << 18 | count): m_v is the word's
 // fixed-point What' row (What' ~ m 2^-s), the product and the sum are exact 64-bit integers
 // (IMAD.WIDE.U32); padding (0) adds 0.
+template <uint32_t kDTs>
 __device__ __forceinline__ unsigned long long entry_mac(uint32_t w, uint32_t row_s, unsigned long long acc) {
-  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + (w >> 16));  // w >> 16 = 4 topic
+  // dt = 18: w >> 16 = 4 topic (one LEA.HI); dt = 16: 4 topic = (w >> 14) & ~3
+  const uint32_t off = (kDTs == 18u) ? (w >> 16) : ((w >> 14) & ~3u);
+  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + off);
 }
 
+template <uint32_t kDTs>
 __device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc, const uint4& a, const uint4& b,
                                                          uint32_t row_s) {
-  acc = entry_mac(a.x, row_s, acc);
-  acc = entry_mac(a.y, row_s, acc);
-  acc = entry_mac(a.z, row_s, acc);
-  acc = entry_mac(a.w, row_s, acc);
-  acc = entry_mac(b.x, row_s, acc);
-  acc = entry_mac(b.y, row_s, acc);
-  acc = entry_mac(b.z, row_s, acc);
-  acc = entry_mac(b.w, row_s, acc);
+  acc = entry_mac<kDTs>(a.x, row_s, acc);
+  acc = entry_mac<kDTs>(a.y, row_s, acc);
+  acc = entry_mac<kDTs>(a.z, row_s, acc);
+  acc = entry_mac<kDTs>(a.w, row_s, acc);
+  acc = entry_mac<kDTs>(b.x, row_s, acc);
+  acc = entry_mac<kDTs>(b.y, row_s, acc);
+  acc = entry_mac<kDTs>(b.z, row_s, acc);
+  acc = entry_mac<kDTs>(b.w, row_s, acc);
   return acc;
 }
 
@@ -841,25 +845,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar_s, uint32_t parity) {
 
 // C1 = D[d][K1] by binary search in the sorted packed row (fallback path: K > 32768 or
 // C1 >= 0x7FFF, where the doc pass cannot carry C1 in the z^i marker).
-template <uint32_t kShift>
-__device__ __forceinline__ uint32_t packed_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
+__device__ __forceinline__ uint32_t packed_count(const uint32_t* E, uint32_t nnz, uint32_t k, uint32_t shift) {
   uint32_t lo = 0, hi = nnz;
   while (lo < hi) {
     const uint32_t mid = (lo + hi) >> 1;
-    if ((__ldg(E + mid) >> kShift) < k) lo = mid + 1u; else hi = mid;
+    if ((__ldg(E + mid) >> shift) < k) lo = mid + 1u; else hi = mid;
   }
   if (lo < nnz) {
     const uint32_t w = __ldg(E + lo);
-    if ((w >> kShift) == k) return w & 0xFFFFu;
+    if ((w >> shift) == k) return w & 0xFFFFu;
   }
   return 0u;
 }
 // D[d][k] of a packed D row / W[v][k] of a packed tail row
-__device__ __forceinline__ uint32_t row_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
-  return packed_count<kDT>(E, nnz, k);
+__device__ __forceinline__ uint32_t row_count(const Dev& d, const uint32_t* E, uint32_t nnz, uint32_t k) {
+  return packed_count(E, nnz, k, d.dt);
 }
 __device__ __forceinline__ uint32_t tail_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
-  return packed_count<16u>(E, nnz, k);
+  return packed_count(E, nnz, k, 16u);
 }
 
 // What[v][k] in fp64 exactly as word-prep / the oracle form it: (W[v][k] + beta) / den_k.
@@ -886,7 +889,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 #pragma unroll 4
   for (uint32_t e = 0; e < nnz; ++e) {
     const uint32_t w = __ldg(E + e);
-    const uint32_t k = d_topic(w);
+    const uint32_t k = d_topic(w, d.dt);
     if (k != K1) Sp = Sp + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
   }
   const double Z = (M + Sp) + rec.Qp;
@@ -902,7 +905,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
     uint32_t last = K1;
     for (uint32_t e = 0; e < nnz; ++e) {
       const uint32_t w = __ldg(E + e);
-      const uint32_t k = d_topic(w);
+      const uint32_t k = d_topic(w, d.dt);
       if (k == K1) continue;
       acc = acc + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
       last = k;
@@ -961,6 +964,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   // checkpoints per segment: one per kSub-entry chunk (kSub = 8: one per 32-byte sector, so a
   // descent walks one sector from registers; kSub = kSegW: one per segment)
   constexpr uint32_t kCk = kSegW / kSub;
+  constexpr uint32_t kDTs = kSegW >= 128u ? kDTLarge : kDTSmall;  // K > 16384 <=> segments >= 128
   constexpr uint32_t kCap = (kSub == 8u ? 2u * kSegCap : kSegCap) / kCk;  // segments per batch
   const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));  // >= 1
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
@@ -1012,7 +1016,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       if (kSegW == 8u) {  // one sector per lane and round (fewer live registers)
         uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa;
         if (e0 < s_nnz) ldg256(p, qa, qb);
-        acc = sector_mac(acc, qa, qb, row_s);
+        acc = sector_mac<kDTs>(acc, qa, qb, row_s);
       } else if (kSegW == 32u && kSub == 8u) {  // four sectors in flight, then accumulated in order
         uint4 q[8];
 #pragma unroll
@@ -1023,18 +1027,18 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         }
 #pragma unroll
         for (uint32_t b = 0; b < 4u; ++b) {
-          acc = sector_mac(acc, q[2 * b], q[2 * b + 1], row_s);
+          acc = sector_mac<kDTs>(acc, q[2 * b], q[2 * b + 1], row_s);
           if (b < 3u) part[b < kCk - 1 ? b : 0] = acc;
         }
       } else {
-#pragma unroll
+#pragma unroll(kSegW <= 64u ? 4 : 2)
         for (uint32_t b = 0; b < kSegW; b += 16u) {
           uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
           if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
           if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
-          acc = sector_mac(acc, qa, qb, row_s);
+          acc = sector_mac<kDTs>(acc, qa, qb, row_s);
           if (kCk == 2u) part[0] = acc;
-          acc = sector_mac(acc, qc, qd, row_s);
+          acc = sector_mac<kDTs>(acc, qc, qd, row_s);
         }
       }
     }
@@ -1094,10 +1098,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (d.zmark) {
       if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
       C1 = zm & 0x7FFFu;
-      if (C1 == d.c1_cap) C1 = row_count(E, s_nnz, K1);  // saturated marker: look C1 up
+      if (C1 == d.c1_cap) C1 = row_count(d, E, s_nnz, K1);  // saturated marker: look C1 up
     } else {
       if (zm != kUnsampled) continue;
-      C1 = row_count(E, s_nnz, K1);
+      C1 = row_count(d, E, s_nnz, K1);
     }
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
     const unsigned long long Spi = nck ? ws.P[c0 + nck - 1u] : 0ull;
@@ -1137,8 +1141,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           for (int e = 0; e < 8; ++e) {
             const uint32_t w = wv[e];
             if (topic == 0xFFFFFFFFu && w != 0u) {
-              const unsigned long long q = entry_mac(w, row_s, pa);
-              if (d_topic(w) != K1 && q > Yf) topic = d_topic(w);
+              const unsigned long long q = entry_mac<kDTs>(w, row_s, pa);
+              if (d_topic(w, kDTs) != K1 && q > Yf) topic = d_topic(w, kDTs);
               else pb = q;
               pa = q;
             }
@@ -1148,10 +1152,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           const uint32_t e1 = min(e0 + kSub, s_nnz);
           for (uint32_t e = e0; e < e1; ++e) {
             const uint32_t w = __ldg(E + e);
-            const unsigned long long q = entry_mac(w, row_s, pa);
+            const unsigned long long q = entry_mac<kDTs>(w, row_s, pa);
             pa = q;
-            if (d_topic(w) != K1 && q > Yf) {
-              topic = d_topic(w);
+            if (d_topic(w, kDTs) != K1 && q > Yf) {
+              topic = d_topic(w, kDTs);
               break;
             }
             pb = q;
@@ -1665,41 +1669,47 @@ __global__ void __launch_bounds__(256) k_tail_rebuild(Dev d, Buf nxt, const uint
 // ---------------------------------------------------------------------------------
 // H8: LLPT, Eq (5) via sum_k (D+alpha) What = S_full + Q_full, one value per (d, v) run.
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double* partial) {
+// kG (large K): the row / chunk prefix live in a per-block HBM scratch (the fp64 row of K =
+// 32768 does not fit shared memory) and the blocks loop over the items.
+template <bool kG>
+__global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double* partial, uint32_t n_items,
+                                                          double* scratch) {
   extern __shared__ __align__(16) unsigned char smem[];
-  double* row = reinterpret_cast<double*>(smem);
+  double* row = kG ? scratch + (size_t)blockIdx.x * (d.Kpad + 2u * d.nch + 1u) : reinterpret_cast<double*>(smem);
   double* T = row + d.Kpad;
   double* CP = T + d.nch;
   __shared__ double s_acc[kLlptWarps];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-  const uint32_t item = blockIdx.x;
-  const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
-  stage_row(d, cur, v, row);
-  chunk_prefix(row, d.nch, T, CP);
-  const double Qfull = d.alpha * CP[d.nch];
-  const double Kalpha = (double)d.K * d.alpha;
-  double acc = 0.0;
-  for (uint32_t r = r0 + warp; r < r1; r += kLlptWarps) {
-    const uint32_t dbase = d.run_dbase[r], len = d.run_len[r];
-    const uint32_t hdr = d.D[dbase];
-    const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
-    const uint32_t* Drow = d.D + dbase + kDHdr;
-    double carry = 0.0;
-    for (uint32_t c = 0; c * 32u < nnz; ++c) {
-      const uint32_t i = c * 32u + lane;
-      const uint32_t e = (i < nnz) ? Drow[i] : 0u;
-      const double w = (i < nnz) ? (double)(e & 0xFFFFu) * row[d_topic(e)] : 0.0;
-      carry = carry + __shfl_sync(kFull, warp_incl_scan(w), 31);
+  for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const uint32_t v = d.item_word[item], r0 = d.item_r0[item], r1 = d.item_r1[item];
+    __syncthreads();  // the previous item's row is no longer read
+    stage_row(d, cur, v, row);
+    chunk_prefix(row, d.nch, T, CP);
+    const double Qfull = d.alpha * CP[d.nch];
+    const double Kalpha = (double)d.K * d.alpha;
+    double acc = 0.0;
+    for (uint32_t r = r0 + warp; r < r1; r += kLlptWarps) {
+      const uint32_t dbase = d.run_dbase[r], len = d.run_len[r];
+      const uint32_t hdr = d.D[dbase];
+      const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
+      const uint32_t* Drow = d.D + dbase + kDHdr;
+      double carry = 0.0;
+      for (uint32_t c = 0; c * 32u < nnz; ++c) {
+        const uint32_t i = c * 32u + lane;
+        const uint32_t e = (i < nnz) ? Drow[i] : 0u;
+        const double w = (i < nnz) ? (double)(e & 0xFFFFu) * row[d_topic(e, d.dt)] : 0.0;
+        carry = carry + __shfl_sync(kFull, warp_incl_scan(w), 31);
+      }
+      const double p = (carry + Qfull) / ((double)L + Kalpha);
+      acc = acc + (double)len * log2(p);
     }
-    const double p = (carry + Qfull) / ((double)L + Kalpha);
-    acc = acc + (double)len * log2(p);
-  }
-  if (lane == 0) s_acc[warp] = acc;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kLlptWarps; ++w) s = s + s_acc[w];
-    partial[item] = s;
+    if (lane == 0) s_acc[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kLlptWarps; ++w) s = s + s_acc[w];
+      partial[item] = s;
+    }
   }
 }
 
@@ -1759,7 +1769,7 @@ __global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) 
     double S = 0.0;
     for (uint32_t e = 0; e < nnz; ++e) {
       const uint32_t w = __ldg(E + e);
-      S = S + (double)(w & 0xFFFFu) * __ldg(wh + d_topic(w));
+      S = S + (double)(w & 0xFFFFu) * __ldg(wh + d_topic(w, d.dt));
     }
     const double Q = __ldg(qp + d.K - 1u);
     const double Z = S + Q;
@@ -1770,7 +1780,7 @@ __global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) 
       double acc = 0.0;
       for (uint32_t e = 0; e < nnz; ++e) {
         const uint32_t w = __ldg(E + e);
-        const uint32_t k = d_topic(w);
+        const uint32_t k = d_topic(w, d.dt);
         acc = acc + (double)(w & 0xFFFFu) * __ldg(wh + k);
         topic = k;
         if (acc > up) break;
@@ -1822,7 +1832,7 @@ __global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32
     double S = 0.0;
     for (uint32_t e = 0; e < nnz; ++e) {
       const uint32_t w = __ldg(E + e);
-      S = S + (double)(w & 0xFFFFu) * wh[d_topic(w)];
+      S = S + (double)(w & 0xFFFFu) * wh[d_topic(w, d.dt)];
     }
     const double Z = S + Q;
     for (uint32_t t = 0; t < len; ++t) {
@@ -1834,7 +1844,7 @@ __global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32
         double acc = 0.0;
         for (uint32_t e = 0; e < nnz; ++e) {
           const uint32_t w = __ldg(E + e);
-          const uint32_t k = d_topic(w);
+          const uint32_t k = d_topic(w, d.dt);
           acc = acc + (double)(w & 0xFFFFu) * wh[k];
           topic = k;
           if (acc > up) break;
@@ -1877,6 +1887,12 @@ __global__ void k_topics_from_input(const uint16_t* in, const uint32_t* perm, ui
 
 }  // namespace
 
+constexpr size_t kLlptSmemMax = 96u * 1024u;  // larger rows: HBM scratch (k_llpt<true>)
+constexpr uint32_t kLlptGrid = 148u * 4u;
+size_t llpt_scratch_doubles(uint32_t K) {
+  const size_t nch = (K + 31) / 32;
+  return kLlptGrid * (nch * 32 + 2 * nch + 1);
+}
 size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
@@ -1958,13 +1974,15 @@ bool two_branch_word_major(uint32_t K) { return tb_item_smem_bytes(K) <= 200u * 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
 static const void* sampler_kernel(uint32_t segw, uint32_t sub, uint32_t qg) {
-  switch (segw) {  // K <= 16384: segment widths 8 .. 64
+  switch (segw) {  // segment widths 8 .. 256 (K <= 65535)
     case 8u: return qg ? (const void*)k_sampler<8u, 8u, true> : (const void*)k_sampler<8u, 8u, false>;
     case 16u: return qg ? (const void*)k_sampler<16u, 8u, true> : (const void*)k_sampler<16u, 8u, false>;
     case 32u:
       if (sub == 8u) return qg ? (const void*)k_sampler<32u, 8u, true> : (const void*)k_sampler<32u, 8u, false>;
       return qg ? (const void*)k_sampler<32u, 32u, true> : (const void*)k_sampler<32u, 32u, false>;
-    default: return qg ? (const void*)k_sampler<64u, 64u, true> : (const void*)k_sampler<64u, 64u, false>;
+    case 64u: return qg ? (const void*)k_sampler<64u, 64u, true> : (const void*)k_sampler<64u, 64u, false>;
+    case 128u: return qg ? (const void*)k_sampler<128u, 128u, true> : (const void*)k_sampler<128u, 128u, false>;
+    default: return qg ? (const void*)k_sampler<256u, 256u, true> : (const void*)k_sampler<256u, 256u, false>;
   }
 }
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
@@ -1992,7 +2010,8 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   if ((e = cudaGetDevice(&dev))) return e;
   if (K <= kWpSmallK && (e = raise_smem(dev, (const void*)k_word_prep_w, (int)word_prep_smem_bytes(K)))) return e;
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
-  if ((e = raise_smem(dev, (const void*)k_llpt, (int)llpt_smem_bytes(K)))) return e;
+  if (llpt_smem_bytes(K) <= kLlptSmemMax && (e = raise_smem(dev, (const void*)k_llpt<false>, (int)llpt_smem_bytes(K))))
+    return e;
   uint32_t segw, sub;
   seg_config(K, &segw, &sub);
   const void* ks = sampler_kernel(segw, sub, sampler_layout(K).qfx_global);
@@ -2082,8 +2101,12 @@ void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, c
   if (Vt) k_tail_rebuild<<<Vt, 256, wcount_smem_bytes(d.K), s>>>(d, nxt, tz_all, off, world, tail_max);
 }
 
-void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s) {
-  if (n_items) k_llpt<<<n_items, kLlptWarps * 32, llpt_smem_bytes(d.K), s>>>(d, cur, partial);
+void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, double* scratch,
+                 cudaStream_t s) {
+  if (n_items && llpt_smem_bytes(d.K) <= kLlptSmemMax)
+    k_llpt<false><<<n_items, kLlptWarps * 32, llpt_smem_bytes(d.K), s>>>(d, cur, partial, n_items, nullptr);
+  else if (n_items)
+    k_llpt<true><<<std::min(n_items, kLlptGrid), kLlptWarps * 32, 0, s>>>(d, cur, partial, n_items, scratch);
   k_sum<<<1, 256, 0, s>>>(partial, n_items, out);
 }
 

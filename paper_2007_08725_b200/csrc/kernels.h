@@ -32,11 +32,14 @@
 namespace ezl {
 
 constexpr uint16_t kUnsampled = 0xFFFFu;  // z^i of a token the sampler must draw (K <= 65535)
-// packed D entry: (topic << kDT) | count, count < 2^16, topic < 2^14 (K <= 16384): the
-// byte offset of topic in a u32 table is then simply entry >> 16 (one LEA.HI per gather)
-constexpr uint32_t kDT = 18;
-__host__ __device__ __forceinline__ uint32_t d_entry(uint32_t k, uint32_t c) { return (k << kDT) | c; }
-__host__ __device__ __forceinline__ uint32_t d_topic(uint32_t w) { return w >> kDT; }
+// packed D entry: (topic << dt) | count, count < 2^16.  dt = 18 when K <= 16384 (topic < 2^14):
+// the byte offset of topic in a u32 table is then simply entry >> 16 (one LEA.HI per gather);
+// dt = 16 for larger K (topic < 2^16)
+constexpr uint32_t kDTSmall = 18, kDTLarge = 16;
+constexpr uint32_t kDTSmallMaxK = 16384;
+__host__ __device__ __forceinline__ uint32_t d_shift(uint32_t K) { return K <= kDTSmallMaxK ? kDTSmall : kDTLarge; }
+__host__ __device__ __forceinline__ uint32_t d_entry(uint32_t k, uint32_t c, uint32_t dt) { return (k << dt) | c; }
+__host__ __device__ __forceinline__ uint32_t d_topic(uint32_t w, uint32_t dt) { return w >> dt; }
 constexpr uint32_t kDHdr = 8;  // header words in front of every packed D row (one 32 B sector)
 #ifndef EZLDA_SEGCAP
 #define EZLDA_SEGCAP 256
@@ -71,6 +74,7 @@ struct Dev {
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
   uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
   uint32_t segsub;  // entries per S' checkpoint chunk (8: one per sector; or segw)
+  uint32_t dt;      // topic shift of the packed D entries (d_shift(K))
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
   // static structure
@@ -125,7 +129,11 @@ bool two_branch_word_major(uint32_t K);
 // H7 (world > 1): global tail rows from every rank's all-gathered word-major tail topics
 void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, const uint32_t* off, uint32_t world,
                          uint64_t tail_max, cudaStream_t s);
-void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, cudaStream_t s);
+// scratch: llpt_scratch_doubles(K) doubles, used when the fp64 row does not fit shared memory
+void launch_llpt(const Dev& d, const Buf& cur, uint32_t n_items, double* partial, double* out, double* scratch,
+                 cudaStream_t s);
+size_t llpt_scratch_doubles(uint32_t K);
+size_t llpt_smem_bytes(uint32_t K);
 
 // ----- setup / IO kernels -----
 void launch_init_topics(const Dev& d, uint16_t* z, cudaStream_t s);

@@ -51,8 +51,12 @@ CONFIGS = {
     "nytimes": CorpusConfig("nytimes", 299_752, 101_636, 332.0, 1.0, 1000),
     "nytimes_k5k": CorpusConfig("nytimes_k5k", 299_752, 101_636, 332.0, 1.0, 5000),
     "nytimes_k10k": CorpusConfig("nytimes_k10k", 299_752, 101_636, 332.0, 1.0, 10000),
+    "nytimes_k32k": CorpusConfig("nytimes_k32k", 299_752, 101_636, 332.0, 1.0, 32768),
     "pubmed": CorpusConfig("pubmed", 8_200_000, 141_043, 90.0, 0.5, 1000),
     "clueweb": CorpusConfig("clueweb", 6_000_000, 1_000_000, 500.0, 1.0, 10000),
+    # one rank's shard of the ClueWeb-shaped corpus at P = 8 (750k docs, ~375 M tokens, the
+    # global vocabulary): the per-GPU workload of the 8 x B200 configuration
+    "clueweb_shard8": CorpusConfig("clueweb_shard8", 750_000, 1_000_000, 500.0, 1.0, 10000),
 }
 
 

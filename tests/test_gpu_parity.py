@@ -151,10 +151,11 @@ def test_long_docs_block_tier_and_large_rows(ez, oracle_mod):
     run_one_step_parity(ez, oracle_mod, w, d, 60, 3000, 1000, 4, check_every=2)
 
 
-@pytest.mark.parametrize("K", [5000, 16384])
+@pytest.mark.parametrize("K", [5000, 16384, 16385, 32768, 40000])
 def test_large_K_paths(ez, oracle_mod, K):
-    """K > 4096: bitonic doc-pass tier, 32/64-entry S' segments, thread-per-word word-prep,
-    HBM slot histograms (K = 16384 is the largest K this build accepts)."""
+    """K > 4096: bitonic doc-pass tier, 32 .. 256-entry S' segments, chunked warp-per-word
+    word-prep, HBM slot histograms and Q' tables; K > 16384: 16-bit topic field in the packed D
+    entries and the HBM-row LLPT kernel; K > 32768: no C1 marker (NEXT-2, P:168 / P:1282)."""
     w, d = planted_corpus_np(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21)
     run_one_step_parity(ez, oracle_mod, w, d, 100, 2000, K, 3, check_every=3)
 
@@ -297,6 +298,8 @@ def test_invalid_arguments(ez):
         ez.EzLDA(w, d, 1, 2, 4, alpha=0.0)
     with pytest.raises(ez.EzLDAError, match="E_RANGE"):
         ez.EzLDA(w, d, 1, 2, 70000)
+    with pytest.raises(ez.EzLDAError, match="E_RANGE"):
+        ez.EzLDA(w, d, 1, 2, 65535)  # valid for the packing, too wide for the sampler's slot
     long_doc = np.zeros(70000, np.uint32)
     with pytest.raises(ez.EzLDAError, match="E_RANGE"):
         ez.EzLDA(long_doc, long_doc, 1, 1, 4)
@@ -360,6 +363,7 @@ TWO_BRANCH_CASES = {
     "K5000": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 5000, 2),
     # K too large for the word's tables in shared memory: HBM tables + doc-major draw + W count
     "K16384_hbm_tables": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 16384, 2),
+    "K32768_hbm_tables": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 32768, 2),
 }
 
 
