@@ -111,18 +111,40 @@ def oracle_sample(cfg, target_tokens: int, seed: int = CORPUS_SEED):
     return w, d, n_docs
 
 
-def time_oracle(cfg, target_tokens: int, iters: int, warmup: int = 0):
+def host_cpu():
+    """nproc and the CPU model of this host (lscpu, else /proc/cpuinfo)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    if model is None and os.path.exists("/proc/cpuinfo"):
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    return os.cpu_count() or 1, model
+
+
+def time_oracle(cfg, target_tokens: int, iters: int, warmup: int = 0, omp: bool = False):
+    """The CPU oracle as it stands on a bounded sample of the workload: tokens/s, tokens, docs,
+    seconds, threads (omp: the OpenMP build over every host core; identical results)."""
     from oracle import oracle
 
-    oracle.build()
+    oracle.build(omp=omp)
     w, d, n_docs = oracle_sample(cfg, target_tokens)
-    orc = oracle.OracleLDA(w, d, n_docs, cfg.V, cfg.K, seed=SAMPLER_SEED)
+    orc = oracle.OracleLDA(w, d, n_docs, cfg.V, cfg.K, seed=SAMPLER_SEED, omp=omp)
     if warmup:
         orc.iterate(warmup)
     t0 = time.perf_counter()
     orc.iterate(iters)
     dt = time.perf_counter() - t0
-    return len(w) * iters / dt, len(w), n_docs, dt
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)) if omp else 1
+    return len(w) * iters / dt, len(w), n_docs, dt, threads
 
 
 def arm_config(cfg, args, world: int) -> dict:
@@ -130,7 +152,7 @@ def arm_config(cfg, args, world: int) -> dict:
     return {"workload": f"{cfg.name}-shaped synthetic LDA", "docs": cfg.n_docs, "V": cfg.V, "K": cfg.K,
             "mean_doc_len": cfg.mean_len, "doc_len_sigma": cfg.sigma, "alpha": cfg.alpha, "beta": cfg.beta,
             "g": args.g, "w_mode": args.w_mode, "split_threshold": args.split or 10000,
-            "exact_draws": bool(args.exact_draws),
+            "exact_draws": bool(args.exact_draws), "doc_block_kb": args.doc_block_kb or 32768,
             "sampler": "two-branch (ESCA)" if args.sampler == 2 else "three-branch",
             "iterations_timed": [args.warmup + 1, args.warmup + args.steps],
             "parallelism": f"doc-partitioned x{world}",
@@ -143,20 +165,37 @@ def run_reference(args, rank, world=1):
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    tps, n, n_docs, dt = time_oracle(cfg, args.ref_tokens, args.steps, args.warmup)
+    tps, n, n_docs, dt, threads = time_oracle(cfg, args.ref_tokens, args.steps, args.warmup, omp=True)
+    nproc, model = host_cpu()
+    conf = arm_config(cfg, args, world)
+    # the sample the oracle actually ran (same recipe, vocabulary, K and doc-length law)
+    conf.update({"workload": f"{cfg.name}-shaped synthetic LDA, bounded oracle sample", "docs": n_docs,
+                 "tokens_per_step": n})
     line = {
         "impl": "reference", "metric": METRIC, "value": tps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": arm_config(cfg, args, world),
-        "cpu_baseline": {"value": tps, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "config": conf,
+        "cpu_baseline": {"value": tps, "unit": UNIT, "cores": threads, "kind": "oracle", "nproc": nproc,
+                         "cpu_model": model,
                          "sample": f"{n} tokens / {n_docs} docs of the {cfg.name}-shaped recipe (V={cfg.V}, "
                                    f"K={cfg.K}), iterations {args.warmup + 1}..{args.warmup + args.steps}, "
-                                   "single-threaded C oracle"},
+                                   f"C oracle OpenMP build on {threads} threads"},
         "e2e": {"value": tps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _fresh_nccl_id(world, rank, dist):
+    """A ncclUniqueId bootstraps one communicator: every multi-rank handle needs a fresh one."""
+    if world <= 1:
+        return None
+    from paper_2007_08725_b200 import lda
+
+    obj = [lda.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
 def main():
@@ -168,10 +207,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=1_000_000, help="oracle sample size for cpu_baseline")
+    ap.add_argument("--cpu-tokens", type=int, default=2_000_000, help="oracle sample size for cpu_baseline")
     ap.add_argument("--cpu-iters", type=int, default=2)
-    ap.add_argument("--ref-tokens", type=int, default=150_000, help="oracle sample size per --impl reference step")
-    ap.add_argument("--doc-block-kb", type=int, default=0, help="sampler L2 tiling (KiB of D rows per block; 0 = off)")
+    ap.add_argument("--ref-tokens", type=int, default=1_000_000, help="oracle sample size per --impl reference step")
+    ap.add_argument("--doc-block-kb", type=int, default=0,
+                    help="sampler L2 tiling: KiB of D rows per doc window (0 = 32 MiB default, 4294967295 = off)")
+    ap.add_argument("--curve-iters", type=int, default=100,
+                    help="iterations of the paper-metric chain (mean tokens/s over 1..N, LLPT curve); 0 = skip")
+    ap.add_argument("--llpt-every", type=int, default=10)
     # ablations (NEXT-3): W storage, S_est depth, large-word split, exact fp64 draws
     ap.add_argument("--w-mode", type=int, default=0, help="0 hybrid W (default), 1 all dense, 2 all sparse")
     ap.add_argument("--g", type=int, default=2, help="S_est depth g in {1,2,3} (Eq 10)")
@@ -310,6 +353,29 @@ def main():
     del ez
     torch.cuda.synchronize()
 
+    # ---- the paper's metric: mean tokens/s over iterations 1..100 and LLPT vs
+    #      iteration (Eq 5), from a fresh chain (iteration times from the per-iteration events)
+    if args.curve_iters:
+        ezc = lda.EzLDA(w, d, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
+                        nccl_id=_fresh_nccl_id(world, rank, dist), token_base=t0, stream=stream.cuda_stream, **knobs)
+        llpt_curve = [[0, ezc.loglik()]]
+        ms_curve = []
+        for it in range(1, args.curve_iters + 1):
+            ezc.iterate(1)
+            st = ezc.stats()
+            ms_curve.append(round(st["ms_total"], 3))
+            if it % args.llpt_every == 0 or it == args.curve_iters:
+                llpt_curve.append([it, ezc.loglik()])
+        del ezc
+        msc = torch.tensor([sum(ms_curve)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(msc, op=dist.ReduceOp.MAX)
+        line["paper_metric"] = {
+            "what": f"mean sampled tokens/s over iterations 1..{args.curve_iters} of a fresh chain (P:1266), "
+                    "per-iteration CUDA-event times (LLPT evaluations excluded)",
+            "mean_tokens_per_s": N_global * args.curve_iters / (float(msc.item()) / 1e3),
+            "ms_per_iteration": ms_curve, "llpt_vs_iteration": llpt_curve}
+
     # ---- end to end through the public API from pinned host buffers (create .. counts)
     if not args.no_e2e:
         hw = torch.empty(w.shape[0], dtype=torch.int32, pin_memory=True)
@@ -320,11 +386,8 @@ def main():
         del w, d
         torch.cuda.empty_cache()
         torch.cuda.synchronize()
-        nccl_id2 = None
-        if world > 1:  # a ncclUniqueId bootstraps one communicator only: fresh id for this instance
-            obj = [lda.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nccl_id2 = obj[0]
+        nccl_id2 = _fresh_nccl_id(world, rank, dist)
+        if world > 1:
             dist.barrier()
         te = time.perf_counter()
         ez2 = lda.EzLDA(hw, hd, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
@@ -344,12 +407,17 @@ def main():
                        "what": f"ezlda_create from pinned host arrays (H2D) + {nsteps} iterations + topics D2H, "
                                "wall clock, setup included"}
 
-    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    # ---- CPU oracle baseline (rank 0, N = 1 only): all host cores (OpenMP build) + one core
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, n, n_docs, dt = time_oracle(cfg, args.cpu_tokens, args.cpu_iters)
-        line["cpu_baseline"] = {"value": tps, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": f"{n} tokens / {n_docs} docs of the {cfg.name}-shaped recipe (V={cfg.V}, "
-                                          f"K={cfg.K}), iterations 1..{args.cpu_iters}, {dt:.1f} s single-threaded C"}
+        nproc, model = host_cpu()
+        tps, n, n_docs, dt, threads = time_oracle(cfg, args.cpu_tokens, args.cpu_iters, omp=True)
+        tps1, n1, nd1, dt1, _ = time_oracle(cfg, args.cpu_tokens // 4, 1)
+        line["cpu_baseline"] = {
+            "value": tps, "unit": UNIT, "cores": threads, "kind": "oracle", "nproc": nproc, "cpu_model": model,
+            "sample": f"{n} tokens / {n_docs} docs of the {cfg.name}-shaped recipe (V={cfg.V}, K={cfg.K}), "
+                      f"iterations 1..{args.cpu_iters}, {dt:.1f} s, C oracle OpenMP build on {threads} threads",
+            "single_thread": {"value": tps1, "unit": UNIT, "cores": 1,
+                              "sample": f"{n1} tokens / {nd1} docs, iteration 1, {dt1:.1f} s"}}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

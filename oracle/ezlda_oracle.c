@@ -454,32 +454,59 @@ int ezlda_oracle_iterate(ezlda_oracle* h, uint32_t n, const int32_t* W_global, c
     if (it == 0 && W_global) memcpy(W, W_global, sizeof(int32_t) * (size_t)h->V * K);
     if (it == 0 && nk_global) memcpy(nk, nk_global, sizeof(int32_t) * K);
     for (uint32_t k = 0; k < K; ++k) den[k] = (double)nk[k] + (double)h->V * h->beta;
-    h->skip_S = h->skip_final = 0;
-    memset(h->branch_hist, 0, sizeof(h->branch_hist));
-    /* step 2-3: per word, then per token of that word */
-    for (uint32_t v = 0; v < h->V; ++v) {
-      if (h->wofs[v] == h->wofs[v + 1]) continue;
-      what_row(h, W, den, v, What);
-      word_rec rec;
-      word_prep(What, K, h->alpha, &rec, P);
-      for (uint64_t q = h->wofs[v]; q < h->wofs[v + 1]; ++q) {
-        const uint64_t t = h->wtok[q];
-        const double u = ezlda_oracle_uniform(h->seed, i, h->tg[t]);
-        if (h->branches == 2) { /* two-branch ESCA draw (Fig 2 text, reading #11); no skip test */
-          double S, Q;
-          znew[t] = (uint16_t)ezlda_oracle_draw_two_branch(D + (size_t)h->doc[t] * K, What, K, h->alpha, u,
-                                                           &S, &Q, NULL, NULL, NULL);
-          h->branch_hist[(u <= S / (S + Q)) ? 2 : 3] += 1;
-          continue;
+    /* step 2-3: per word, then per token of that word.  Every draw reads only the snapshot
+     * and writes its own znew entry, so the words are independent: the OpenMP build
+     * (libezlda_oracle_omp.so, bench.py's all-core CPU leg) splits them over threads with
+     * identical results; the default build compiles the pragmas away. */
+    uint64_t skS = 0, skF = 0, bh0 = 0, bh1 = 0, bh2 = 0, bh3 = 0;
+#ifdef _OPENMP
+#pragma omp parallel reduction(+ : skS, skF, bh0, bh1, bh2, bh3)
+#endif
+    {
+      double* What_t = What;
+      double* P_t = P;
+#ifdef _OPENMP
+      What_t = (double*)malloc(sizeof(double) * K);
+      P_t = (double*)malloc(sizeof(double) * K);
+#pragma omp for schedule(dynamic, 16)
+#endif
+      for (uint32_t v = 0; v < h->V; ++v) {
+        if (h->wofs[v] == h->wofs[v + 1]) continue;
+        what_row(h, W, den, v, What_t);
+        word_rec rec;
+        word_prep(What_t, K, h->alpha, &rec, P_t);
+        for (uint64_t q = h->wofs[v]; q < h->wofs[v + 1]; ++q) {
+          const uint64_t t = h->wtok[q];
+          const double u = ezlda_oracle_uniform(h->seed, i, h->tg[t]);
+          if (h->branches == 2) { /* two-branch ESCA draw (Fig 2 text, reading #11); no skip test */
+            double S, Q;
+            znew[t] = (uint16_t)ezlda_oracle_draw_two_branch(D + (size_t)h->doc[t] * K, What_t, K, h->alpha, u,
+                                                             &S, &Q, NULL, NULL, NULL);
+            if (u <= S / (S + Q)) bh2 += 1; else bh3 += 1;
+            continue;
+          }
+          ezlda_oracle_draw_detail det;
+          token_draw(&rec, P_t, What_t, D + (size_t)h->doc[t] * K, K, h->alpha, h->g, u, &det);
+          znew[t] = (uint16_t)det.topic;
+          if (det.branch == 0) bh0 += 1;
+          else if (det.branch == 1) bh1 += 1;
+          else if (det.branch == 2) bh2 += 1;
+          else bh3 += 1;
+          if (det.branch == 0) skS += 1;
+          if (det.branch <= 1) skF += 1;
         }
-        ezlda_oracle_draw_detail det;
-        token_draw(&rec, P, What, D + (size_t)h->doc[t] * K, K, h->alpha, h->g, u, &det);
-        znew[t] = (uint16_t)det.topic;
-        h->branch_hist[det.branch] += 1;
-        if (det.branch == 0) h->skip_S += 1;
-        if (det.branch <= 1) h->skip_final += 1;
       }
+#ifdef _OPENMP
+      free(What_t);
+      free(P_t);
+#endif
     }
+    h->skip_S = skS;
+    h->skip_final = skF;
+    h->branch_hist[0] = bh0;
+    h->branch_hist[1] = bh1;
+    h->branch_hist[2] = bh2;
+    h->branch_hist[3] = bh3;
     /* step 4: commit all topics simultaneously (snapshot, reading #13) */
     memcpy(h->z, znew, sizeof(uint16_t) * h->N);
     h->iterations = i;

@@ -16,17 +16,20 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "ezlda_oracle.c")
 LIB = os.path.join(HERE, "libezlda_oracle.so")
+LIB_OMP = os.path.join(HERE, "libezlda_oracle_omp.so")  # the same source with -fopenmp (all-core timing)
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (-O2 -ffp-contract=off: no FMA contraction)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle with gcc (-O2 -ffp-contract=off: no FMA contraction); omp=True builds
+    the OpenMP variant (words split over threads; identical results)."""
+    lib = LIB_OMP if omp else LIB
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(
         os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "ezlda_oracle.h"))
     ):
         cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-Wall", "-o", LIB, SRC, "-lm"]
+               "-Wall", *(["-fopenmp"] if omp else []), "-o", lib, SRC, "-lm"]
         subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 class DrawDetail(C.Structure):
@@ -46,51 +49,61 @@ class DrawDetail(C.Structure):
 
 
 _lib = None
+_libs = {}
 
 
-def lib():
+def lib(omp: bool = False):
+    """The oracle library (omp=True: the OpenMP build, loaded side by side)."""
     global _lib
+    if omp:
+        if "omp" not in _libs:
+            build(omp=True)
+            _libs["omp"] = _declare(C.CDLL(LIB_OMP))
+        return _libs["omp"]
     if _lib is None:
         build()
-        L = C.CDLL(LIB)
-        P = C.POINTER
-        L.ezlda_oracle_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
-        L.ezlda_oracle_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64]
-        L.ezlda_oracle_uniform.restype = C.c_double
-        L.ezlda_oracle_init_topic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]
-        L.ezlda_oracle_init_topic.restype = C.c_uint32
-        L.ezlda_oracle_draw_three_branch.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double,
-                                                     C.c_uint32, C.c_double, P(DrawDetail)]
-        L.ezlda_oracle_draw_grid.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double, C.c_uint32,
-                                             P(C.c_double), C.c_uint64, P(C.c_uint32), P(C.c_int32)]
-        L.ezlda_oracle_what.argtypes = [C.c_void_p, C.c_uint32, P(C.c_int32), P(C.c_int32), P(C.c_double)]
-        L.ezlda_oracle_draw_two_branch.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double,
-                                                   C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
-                                                   P(C.c_double), P(C.c_double)]
-        L.ezlda_oracle_draw_two_branch.restype = C.c_uint32
-        L.ezlda_oracle_what_row.argtypes = [P(C.c_int32), P(C.c_int32), C.c_uint32, C.c_uint32, C.c_double,
-                                            P(C.c_double)]
-        L.ezlda_oracle_what_row.restype = None
-        L.ezlda_oracle_set_sampler.argtypes = [C.c_void_p, C.c_uint32]
-        L.ezlda_oracle_set_sampler.restype = C.c_int
-        L.ezlda_oracle_inverted_index.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32,
-                                                  P(C.c_uint64), P(C.c_uint64)]
-        L.ezlda_oracle_create.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32, C.c_uint32,
-                                          C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_uint32,
-                                          C.c_uint64, P(C.c_void_p)]
-        L.ezlda_oracle_destroy.argtypes = [C.c_void_p]
-        L.ezlda_oracle_token_index.argtypes = [C.c_void_p, P(C.c_uint64)]
-        L.ezlda_oracle_set_topics.argtypes = [C.c_void_p, P(C.c_uint16), C.c_uint32]
-        L.ezlda_oracle_topics.argtypes = [C.c_void_p, P(C.c_uint16)]
-        L.ezlda_oracle_iterations.argtypes = [C.c_void_p]
-        L.ezlda_oracle_iterations.restype = C.c_uint32
-        L.ezlda_oracle_iterate.argtypes = [C.c_void_p, C.c_uint32, P(C.c_int32), P(C.c_int32)]
-        L.ezlda_oracle_counts.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32)]
-        L.ezlda_oracle_loglik.argtypes = [C.c_void_p, C.c_int, P(C.c_int32), P(C.c_int32), P(C.c_double),
-                                          P(C.c_double)]
-        L.ezlda_oracle_last_stats.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]
-        _lib = L
+        _lib = _declare(C.CDLL(LIB))
     return _lib
+
+
+def _declare(L):
+    P = C.POINTER
+    L.ezlda_oracle_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+    L.ezlda_oracle_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64]
+    L.ezlda_oracle_uniform.restype = C.c_double
+    L.ezlda_oracle_init_topic.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32]
+    L.ezlda_oracle_init_topic.restype = C.c_uint32
+    L.ezlda_oracle_draw_three_branch.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double,
+                                                 C.c_uint32, C.c_double, P(DrawDetail)]
+    L.ezlda_oracle_draw_grid.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double, C.c_uint32,
+                                         P(C.c_double), C.c_uint64, P(C.c_uint32), P(C.c_int32)]
+    L.ezlda_oracle_what.argtypes = [C.c_void_p, C.c_uint32, P(C.c_int32), P(C.c_int32), P(C.c_double)]
+    L.ezlda_oracle_draw_two_branch.argtypes = [P(C.c_int32), P(C.c_double), C.c_uint32, C.c_double,
+                                               C.c_double, P(C.c_double), P(C.c_double), P(C.c_double),
+                                               P(C.c_double), P(C.c_double)]
+    L.ezlda_oracle_draw_two_branch.restype = C.c_uint32
+    L.ezlda_oracle_what_row.argtypes = [P(C.c_int32), P(C.c_int32), C.c_uint32, C.c_uint32, C.c_double,
+                                        P(C.c_double)]
+    L.ezlda_oracle_what_row.restype = None
+    L.ezlda_oracle_set_sampler.argtypes = [C.c_void_p, C.c_uint32]
+    L.ezlda_oracle_set_sampler.restype = C.c_int
+    L.ezlda_oracle_inverted_index.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32,
+                                              P(C.c_uint64), P(C.c_uint64)]
+    L.ezlda_oracle_create.argtypes = [P(C.c_uint32), P(C.c_uint32), C.c_uint64, C.c_uint32, C.c_uint32,
+                                      C.c_uint32, C.c_double, C.c_double, C.c_uint64, C.c_uint32,
+                                      C.c_uint64, P(C.c_void_p)]
+    L.ezlda_oracle_destroy.argtypes = [C.c_void_p]
+    L.ezlda_oracle_token_index.argtypes = [C.c_void_p, P(C.c_uint64)]
+    L.ezlda_oracle_set_topics.argtypes = [C.c_void_p, P(C.c_uint16), C.c_uint32]
+    L.ezlda_oracle_topics.argtypes = [C.c_void_p, P(C.c_uint16)]
+    L.ezlda_oracle_iterations.argtypes = [C.c_void_p]
+    L.ezlda_oracle_iterations.restype = C.c_uint32
+    L.ezlda_oracle_iterate.argtypes = [C.c_void_p, C.c_uint32, P(C.c_int32), P(C.c_int32)]
+    L.ezlda_oracle_counts.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32)]
+    L.ezlda_oracle_loglik.argtypes = [C.c_void_p, C.c_int, P(C.c_int32), P(C.c_int32), P(C.c_double),
+                                      P(C.c_double)]
+    L.ezlda_oracle_last_stats.argtypes = [C.c_void_p, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]
+    return L
 
 
 def _ptr(a: np.ndarray | None, ctype):
@@ -176,7 +189,9 @@ class OracleLDA:
     """The plain CPU chain: create / iterate / topics / counts / loglik."""
 
     def __init__(self, word_ids, doc_ids, n_docs: int, V: int, K: int, alpha: float | None = None,
-                 beta: float = 0.01, seed: int = 1, g: int = 2, token_base: int = 0, branches: int = 3):
+                 beta: float = 0.01, seed: int = 1, g: int = 2, token_base: int = 0, branches: int = 3,
+                 omp: bool = False):
+        self._L = lib(omp)  # omp: the OpenMP build (all host cores), identical results
         self.word = np.ascontiguousarray(word_ids, dtype=np.uint32)
         self.doc = np.ascontiguousarray(doc_ids, dtype=np.uint32)
         self.N = len(self.word)
@@ -184,51 +199,51 @@ class OracleLDA:
         self.alpha = 50.0 / K if alpha is None else alpha
         self.beta = beta
         h = C.c_void_p()
-        rc = lib().ezlda_oracle_create(_ptr(self.word, C.c_uint32), _ptr(self.doc, C.c_uint32), self.N, n_docs,
+        rc = self._L.ezlda_oracle_create(_ptr(self.word, C.c_uint32), _ptr(self.doc, C.c_uint32), self.N, n_docs,
                                        V, K, self.alpha, beta, seed, g, token_base, C.byref(h))
         if rc:
             raise ValueError(f"ezlda_oracle_create rc={rc}")
         self._h = h
-        if lib().ezlda_oracle_set_sampler(h, branches):
+        if self._L.ezlda_oracle_set_sampler(h, branches):
             raise ValueError("branches must be 2 or 3")
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and _lib is not None:
-            _lib.ezlda_oracle_destroy(h)
+        if h is not None and getattr(self, "_L", None) is not None:
+            self._L.ezlda_oracle_destroy(h)
             self._h = None
 
     @property
     def iterations(self) -> int:
-        return lib().ezlda_oracle_iterations(self._h)
+        return self._L.ezlda_oracle_iterations(self._h)
 
     def token_index(self) -> np.ndarray:
         out = np.zeros(self.N, dtype=np.uint64)
-        lib().ezlda_oracle_token_index(self._h, _ptr(out, C.c_uint64))
+        self._L.ezlda_oracle_token_index(self._h, _ptr(out, C.c_uint64))
         return out
 
     def what(self, v: int, W_global=None, nk_global=None) -> np.ndarray:
         Wg = None if W_global is None else np.ascontiguousarray(W_global, dtype=np.int32)
         ng = None if nk_global is None else np.ascontiguousarray(nk_global, dtype=np.int32)
         row = np.zeros(self.K)
-        if lib().ezlda_oracle_what(self._h, v, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32), _ptr(row, C.c_double)):
+        if self._L.ezlda_oracle_what(self._h, v, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32), _ptr(row, C.c_double)):
             raise ValueError("word out of range")
         return row
 
     def set_topics(self, topics, iterations_done: int) -> None:
         z = np.ascontiguousarray(topics, dtype=np.uint16)
-        if lib().ezlda_oracle_set_topics(self._h, _ptr(z, C.c_uint16), iterations_done):
+        if self._L.ezlda_oracle_set_topics(self._h, _ptr(z, C.c_uint16), iterations_done):
             raise ValueError("topic out of range")
 
     def topics(self) -> np.ndarray:
         z = np.zeros(self.N, dtype=np.uint16)
-        lib().ezlda_oracle_topics(self._h, _ptr(z, C.c_uint16))
+        self._L.ezlda_oracle_topics(self._h, _ptr(z, C.c_uint16))
         return z
 
     def iterate(self, n: int = 1, W_global=None, nk_global=None) -> None:
         Wg = None if W_global is None else np.ascontiguousarray(W_global, dtype=np.int32)
         ng = None if nk_global is None else np.ascontiguousarray(nk_global, dtype=np.int32)
-        rc = lib().ezlda_oracle_iterate(self._h, n, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32))
+        rc = self._L.ezlda_oracle_iterate(self._h, n, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32))
         if rc:
             raise RuntimeError(f"ezlda_oracle_iterate rc={rc}")
 
@@ -236,14 +251,14 @@ class OracleLDA:
         D = np.zeros((self.n_docs, self.K), dtype=np.int32)
         W = np.zeros((self.V, self.K), dtype=np.int32)
         nk = np.zeros(self.K, dtype=np.int32)
-        lib().ezlda_oracle_counts(self._h, _ptr(D, C.c_int32), _ptr(W, C.c_int32), _ptr(nk, C.c_int32))
+        self._L.ezlda_oracle_counts(self._h, _ptr(D, C.c_int32), _ptr(W, C.c_int32), _ptr(nk, C.c_int32))
         return D, W, nk
 
     def loglik(self, method: int = 1, W_global=None, nk_global=None, return_sum: bool = False):
         Wg = None if W_global is None else np.ascontiguousarray(W_global, dtype=np.int32)
         ng = None if nk_global is None else np.ascontiguousarray(nk_global, dtype=np.int32)
         out, s = C.c_double(), C.c_double()
-        rc = lib().ezlda_oracle_loglik(self._h, method, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32), C.byref(out),
+        rc = self._L.ezlda_oracle_loglik(self._h, method, _ptr(Wg, C.c_int32), _ptr(ng, C.c_int32), C.byref(out),
                                        C.byref(s))
         if rc:
             raise RuntimeError(f"ezlda_oracle_loglik rc={rc}")
@@ -252,5 +267,5 @@ class OracleLDA:
     def last_stats(self) -> dict:
         a, b = C.c_uint64(), C.c_uint64()
         hist = (C.c_uint64 * 4)()
-        lib().ezlda_oracle_last_stats(self._h, C.byref(a), C.byref(b), hist)
+        self._L.ezlda_oracle_last_stats(self._h, C.byref(a), C.byref(b), hist)
         return {"skip_S": a.value, "skip_final": b.value, "branch_hist": list(hist)}

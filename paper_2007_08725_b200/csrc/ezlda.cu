@@ -515,7 +515,7 @@ void fill_dev(ezlda* h) {
   d.Kpad = d.nch * 32;
   d.Vd = h->Vd;
   d.rs = ezl::wrow_stride(h->K);
-  ezl::seg_config(h->K, &d.segw, &d.segsub);
+  ezl::seg_config(h->K, &d.segw, &d.segsub, &d.segfb);
   d.dt = ezl::d_shift(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
   d.c1_cap = (h->debug_flags & EZLDA_DEBUG_C1_LOOKUP) ? 0u : 0x7FFFu;

@@ -933,7 +933,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
 // of the fast path (x vs M, x vs M + S', the S' and Q' descents) is taken only if it holds
 // with a margin bounding that error (2 L_d 2^-s + 4e-15 Z); otherwise the token is redrawn
 // by exact_draw.  Either way the topic equals the oracle's fp64 decision.
-template <uint32_t kSegW, uint32_t kSub, bool kQG>
+template <uint32_t kSegW, uint32_t kSub, uint32_t kDTs, bool kQG>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
                                                  uint32_t v, uint32_t row_s, const uint32_t* qfx, const uint32_t* ce,
                                                  const double* scl,
@@ -964,9 +964,9 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   // checkpoints per segment: one per kSub-entry chunk (kSub = 8: one per 32-byte sector, so a
   // descent walks one sector from registers; kSub = kSegW: one per segment)
   constexpr uint32_t kCk = kSegW / kSub;
-  constexpr uint32_t kDTs = kSegW >= 128u ? kDTLarge : kDTSmall;  // K > 16384 <=> segments >= 128
   constexpr uint32_t kCap = (kSub == 8u ? 2u * kSegCap : kSegCap) / kCk;  // segments per batch
-  const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));  // >= 1
+  const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));
+  if (nb == 0) return 0;  // the first run alone exceeds a batch: the caller takes its wide-segment path
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
   const uint32_t soff = sincl - nseg;
   tincl = (lane < nb) ? len : 0u;
@@ -1001,6 +1001,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   //      fixed-point What' row), combined by a segmented warp scan (+ carry across rounds).
   //      Checkpoints: P[kCk g + i] = P(before g) + (chunks 0..i of g); the last one is
   //      P(end of g), and S' = the run's last checkpoint.
+  static_assert(kCk == 1u || kCk == 2u, "checkpoints per segment");
   unsigned long long carry = 0ull;
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
     const uint32_t g = B0 + lane;
@@ -1011,26 +1012,9 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t e0 = (g - s_soff) * kSegW;
     const uint32_t* p = d.D + s_ebase + e0;
     unsigned long long acc = 0ull;
-    unsigned long long part[kCk > 1 ? kCk - 1 : 1];  // running sums after chunks 0 .. kCk-2
+    unsigned long long part[1] = {0ull};  // running sum after the first sector (kCk == 2)
     if (g < T) {
-      if (kSegW == 8u) {  // one sector per lane and round (fewer live registers)
-        uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa;
-        if (e0 < s_nnz) ldg256(p, qa, qb);
-        acc = sector_mac<kDTs>(acc, qa, qb, row_s);
-      } else if (kSegW == 32u && kSub == 8u) {  // four sectors in flight, then accumulated in order
-        uint4 q[8];
-#pragma unroll
-        for (uint32_t b = 0; b < 4u; ++b) {
-          q[2 * b] = make_uint4(0u, 0u, 0u, 0u);
-          q[2 * b + 1] = q[2 * b];
-          if (e0 + 8u * b < s_nnz) ldg256(p + 8u * b, q[2 * b], q[2 * b + 1]);
-        }
-#pragma unroll
-        for (uint32_t b = 0; b < 4u; ++b) {
-          acc = sector_mac<kDTs>(acc, q[2 * b], q[2 * b + 1], row_s);
-          if (b < 3u) part[b < kCk - 1 ? b : 0] = acc;
-        }
-      } else {
+      {
 #pragma unroll(kSegW <= 64u ? 4 : 2)
         for (uint32_t b = 0; b < kSegW; b += 16u) {
           uint4 qa = make_uint4(0u, 0u, 0u, 0u), qb = qa, qc = qa, qd = qa;
@@ -1056,20 +1040,11 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         ws.P[g] = acc;
       } else {
         const unsigned long long excl = acc - tot;  // prefix before segment g
-        if (kCk == 2u) {  // the two checkpoints of a segment are adjacent: one 16-byte store
-          ulonglong2 pr;
-          pr.x = excl + part[0];
-          pr.y = acc;
-          *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
-        } else {
-          ulonglong2 pr0, pr1;
-          pr0.x = excl + part[0];
-          pr0.y = excl + part[kCk > 2 ? 1 : 0];
-          pr1.x = excl + part[kCk > 3 ? 2 : 0];
-          pr1.y = acc;
-          *reinterpret_cast<ulonglong2*>(ws.P + kCk * g) = pr0;
-          *reinterpret_cast<ulonglong2*>(ws.P + kCk * g + 2u) = pr1;
-        }
+        // kCk == 2: the two checkpoints of a segment are adjacent: one 16-byte store
+        ulonglong2 pr;
+        pr.x = excl + part[0];
+        pr.y = acc;
+        *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
       }
     }
     carry = __shfl_sync(kFull, acc, 31);
@@ -1148,17 +1123,25 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             }
           }
         } else {
+          // walk the chunk two sectors (16 entries) at a time from registers: one memory
+          // round trip per 16 entries instead of one per entry
           const uint32_t e0 = (a - c0) * kSub;
-          const uint32_t e1 = min(e0 + kSub, s_nnz);
-          for (uint32_t e = e0; e < e1; ++e) {
-            const uint32_t w = __ldg(E + e);
-            const unsigned long long q = entry_mac<kDTs>(w, row_s, pa);
-            pa = q;
-            if (d_topic(w, kDTs) != K1 && q > Yf) {
-              topic = d_topic(w, kDTs);
-              break;
+          for (uint32_t eb = e0; eb < e0 + kSub && eb < s_nnz && topic == 0xFFFFFFFFu; eb += 16u) {
+            uint4 qa, qb, qc = make_uint4(0u, 0u, 0u, 0u), qd = qc;
+            ldg256(E + eb, qa, qb);
+            if (eb + 8u < s_nnz) ldg256(E + eb + 8u, qc, qd);
+            const uint32_t wv[16] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w,
+                                     qc.x, qc.y, qc.z, qc.w, qd.x, qd.y, qd.z, qd.w};
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t w = wv[e];
+              if (topic == 0xFFFFFFFFu && w != 0u) {  // w == 0: zero padding past nnz
+                const unsigned long long q = entry_mac<kDTs>(w, row_s, pa);
+                if (d_topic(w, kDTs) != K1 && q > Yf) topic = d_topic(w, kDTs);
+                else pb = q;
+                pa = q;
+              }
             }
-            pb = q;
           }
         }
         // certify: the candidate's interval [pb, pa) holds y with margin on both sides
@@ -1464,7 +1447,7 @@ __host__ __device__ __forceinline__ uint32_t sampler_ctl_bytes() {
 
 // one kernel per (S' segment width, Q' table placement): each gets the register allocation
 // of its own path only
-template <uint32_t kSegW, uint32_t kSub, bool kQG>
+template <uint32_t kSegW, uint32_t kSub, uint32_t kFbW, uint32_t kDTs, bool kQG>
 __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(Dev d, Buf cur, Buf nxt, uint32_t iter,
                                                                   uint32_t n_items) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1563,8 +1546,11 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
-      const uint32_t nb = sample_batch<kSegW, kSub, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, &c.qp, hist, ws, qn,
-                                                         iter, rc);
+      uint32_t nb = sample_batch<kSegW, kSub, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, &c.qp, hist, ws,
+                                                         qn, iter, rc);
+      if (kFbW && nb == 0)  // a run with more than kSegCap x 16 nonzeros (large K only): wide segments
+        nb = sample_batch<kFbW ? kFbW : 16u, kFbW ? kFbW : 16u, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl,
+                                                                          &c.qp, hist, ws, qn, iter, rc);
 
       // drop the processed runs from the queue
       const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
@@ -1904,27 +1890,22 @@ uint32_t wrow_stride(uint32_t K) {  // m | scales | qfx | ce | QP (doubles)
 #ifndef EZLDA_SEG_MIN
 #define EZLDA_SEG_MIN 16
 #endif
-#ifndef EZLDA_SEG_QUAD
-#define EZLDA_SEG_QUAD 0  // 1: 32-entry segments with a checkpoint per sector for K <= 4096
-#endif
-// S' segment layout of K: entries per segment (a power of two >= EZLDA_SEG_MIN with
-// K <= segments-per-batch x width, so one run always fits a batch) and entries per checkpoint
-// chunk (8 = one per 32-byte sector up to 16-entry segments, or with EZLDA_SEG_QUAD)
-void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub) {
-  if (EZLDA_SEG_QUAD && K <= (2u * kSegCap / 4u) * 32u) {
-    *segw = 32u;
+// S' segment layout of K: 16-entry segments (two 32-byte sectors per lane and round) with a
+// checkpoint per sector (K <= 4096: every row fits one batch of kSegCap segments) or per
+// segment (K > 4096: the descent walks two sectors from registers); runs longer than kSegCap x
+// 16 nonzeros (large K only) take a fallback with fb-entry segments, fb a power of two with
+// K <= kSegCap x fb.
+void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb) {
+  *segw = 16u;
+  if (K <= kSegCap * 16u) {
     *sub = 8u;
+    *fb = 0u;
     return;
   }
-  uint32_t w = EZLDA_SEG_MIN;
-  while (w * (w == 8u ? 2u * kSegCap : kSegCap) < K) w <<= 1;
-  *segw = w;
-  *sub = w <= 16u ? 8u : w;
-}
-uint32_t seg_width(uint32_t K) {
-  uint32_t w, sb;
-  seg_config(K, &w, &sb);
-  return w;
+  *sub = 16u;
+  uint32_t w = 32u;
+  while (w * kSegCap < K) w <<= 1;
+  *fb = w;
 }
 constexpr size_t kMaxSmem = 227u * 1024u;
 // shared-memory layout of the sampler block: kMaxSlots SlotCtl | nslots x (slot head [+ hist])
@@ -1933,8 +1914,8 @@ constexpr size_t kMaxSmem = 227u * 1024u;
 SamplerLayout sampler_layout(uint32_t K) {
   SamplerLayout L{};
   const uint32_t Kpad = (K + 31) / 32 * 32;
-  uint32_t segw, sub;
-  seg_config(K, &segw, &sub);
+  uint32_t segw, sub, fb;
+  seg_config(K, &segw, &sub, &fb);
   L.ws_bytes = (sub == 8u ? 2u * kSegCap : kSegCap) * 8u + 4u * kQueue;
   const size_t fixed = sampler_ctl_bytes() + (size_t)kSampWarpsP * L.ws_bytes;
   // prefer layouts that keep EZLDA_SAMP_MINB blocks per SM (the register budget assumes it)
@@ -1973,16 +1954,19 @@ bool two_branch_word_major(uint32_t K) { return tb_item_smem_bytes(K) <= 200u * 
 
 size_t doc_block_smem_bytes(uint32_t K) { return (size_t)((K + 31) / 32) * 32 * 4; }
 
-static const void* sampler_kernel(uint32_t segw, uint32_t sub, uint32_t qg) {
-  switch (segw) {  // segment widths 8 .. 256 (K <= 65535)
-    case 8u: return qg ? (const void*)k_sampler<8u, 8u, true> : (const void*)k_sampler<8u, 8u, false>;
-    case 16u: return qg ? (const void*)k_sampler<16u, 8u, true> : (const void*)k_sampler<16u, 8u, false>;
-    case 32u:
-      if (sub == 8u) return qg ? (const void*)k_sampler<32u, 8u, true> : (const void*)k_sampler<32u, 8u, false>;
-      return qg ? (const void*)k_sampler<32u, 32u, true> : (const void*)k_sampler<32u, 32u, false>;
-    case 64u: return qg ? (const void*)k_sampler<64u, 64u, true> : (const void*)k_sampler<64u, 64u, false>;
-    case 128u: return qg ? (const void*)k_sampler<128u, 128u, true> : (const void*)k_sampler<128u, 128u, false>;
-    default: return qg ? (const void*)k_sampler<256u, 256u, true> : (const void*)k_sampler<256u, 256u, false>;
+template <uint32_t kFbW, uint32_t kDTs>
+static const void* sampler_kernel_fb(uint32_t qg) {
+  return qg ? (const void*)k_sampler<16u, 16u, kFbW, kDTs, true> : (const void*)k_sampler<16u, 16u, kFbW, kDTs, false>;
+}
+static const void* sampler_kernel(uint32_t K, uint32_t qg) {
+  uint32_t segw, sub, fb;
+  seg_config(K, &segw, &sub, &fb);
+  if (fb == 0u) return qg ? (const void*)k_sampler<16u, 8u, 0u, kDTSmall, true> : (const void*)k_sampler<16u, 8u, 0u, kDTSmall, false>;
+  switch (fb) {  // K > 4096: fallback segment width 32 .. 256 (K <= 65535)
+    case 32u: return sampler_kernel_fb<32u, kDTSmall>(qg);
+    case 64u: return sampler_kernel_fb<64u, kDTSmall>(qg);
+    case 128u: return sampler_kernel_fb<128u, kDTLarge>(qg);
+    default: return sampler_kernel_fb<256u, kDTLarge>(qg);
   }
 }
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
@@ -2012,9 +1996,7 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   const int sp = (int)sampler_smem_bytes(K), db = (int)doc_block_smem_bytes(K);
   if (llpt_smem_bytes(K) <= kLlptSmemMax && (e = raise_smem(dev, (const void*)k_llpt<false>, (int)llpt_smem_bytes(K))))
     return e;
-  uint32_t segw, sub;
-  seg_config(K, &segw, &sub);
-  const void* ks = sampler_kernel(segw, sub, sampler_layout(K).qfx_global);
+  const void* ks = sampler_kernel(K, sampler_layout(K).qfx_global);
   if ((e = raise_smem(dev, ks, sp))) return e;
   if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev))) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks, kSampWarpsP * 32, (size_t)sp))) return e;
@@ -2077,7 +2059,7 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
     k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, cur, nxt);
   else
     {
-      const void* ks = sampler_kernel(d.segw, d.segsub, d.qfx_global);
+      const void* ks = sampler_kernel(d.K, d.qfx_global);
       const uint32_t grid = std::min<uint32_t>(n_items, d.sampler_grid);
       void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
       cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);

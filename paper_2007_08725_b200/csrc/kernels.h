@@ -74,6 +74,7 @@ struct Dev {
   uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
   uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
   uint32_t segsub;  // entries per S' checkpoint chunk (8: one per sector; or segw)
+  uint32_t segfb;   // fallback segment width for runs longer than kSegCap x segw (0: none)
   uint32_t dt;      // topic shift of the packed D entries (d_shift(K))
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
@@ -149,8 +150,7 @@ struct SamplerLayout {
 SamplerLayout sampler_layout(uint32_t K);
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad);  // doubles per slot of qp_scratch
 uint32_t wrow_stride(uint32_t K);
-uint32_t seg_width(uint32_t K);
-void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub);
+void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb);
 size_t doc_block_smem_bytes(uint32_t K);
 // Raise the dynamic shared-memory limits of the kernels K needs (never lowered: handles with
 // different K may be alive at once) and return this K's persistent sampler grid in *grid.

@@ -160,6 +160,15 @@ def test_large_K_paths(ez, oracle_mod, K):
     run_one_step_parity(ez, oracle_mod, w, d, 100, 2000, K, 3, check_every=3)
 
 
+@pytest.mark.parametrize("K", [8000, 16384, 32768])
+def test_wide_segment_fallback(ez, oracle_mod, K):
+    """K > 4096 with documents holding more than 4096 distinct topics (256 segments of 16): those
+    runs take the wide-segment fallback of the sampler (32 .. 256-entry segments)."""
+    w, d = planted_corpus_np(n_docs=30, V=2000, mean_len=3000.0, sigma=0.8, K_true=50, seed=33)
+    assert np.bincount(d).max() > 8000
+    run_one_step_parity(ez, oracle_mod, w, d, 30, 2000, K, 2, check_every=2)
+
+
 def test_exact_draws_knob_identical(ez, oracle_mod, small):
     """exact_draws=1 sends every sampled token through the fp64 path: topics identical to
     the default certified fixed-point path and to the oracle; the default path redraws few tokens."""

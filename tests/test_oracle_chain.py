@@ -223,3 +223,17 @@ def test_iterate_is_per_token_draw_on_recounted_snapshot(oracle_mod, tiny, branc
         else:
             topic = oracle_mod.draw_two_branch(Db[d[t]], whats[v], h.alpha, u)["topic"]
         assert topic == z_new[t], (t, topic, z_new[t])
+
+
+@pytest.mark.parametrize("branches", [3, 2])
+def test_openmp_build_is_identical(oracle_mod, tiny, branches):
+    """The OpenMP build of the oracle (bench.py's all-core CPU leg) splits the per-word loop
+    over threads; every draw reads only the snapshot, so topics and counters are identical."""
+    w, d = tiny
+    a = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 16, branches=branches)
+    b = oracle_mod.OracleLDA(w, d, TINY["n_docs"], TINY["V"], 16, branches=branches, omp=True)
+    for _ in range(4):
+        a.iterate(1)
+        b.iterate(1)
+        assert np.array_equal(a.topics(), b.topics())
+        assert a.last_stats() == b.last_stats()
