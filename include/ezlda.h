@@ -98,6 +98,13 @@ typedef struct {
                              /* Every rank of a key must pass the same world (else E_INVALID)*/
   uint32_t debug_flags;      /* test hooks forcing rarely taken paths (EZLDA_DEBUG_*); the   */
                              /* topics do not depend on them                                */
+  uint32_t schedule;         /* sampler work schedule (hierarchical balancing): */
+                             /* 0: items split every split_threshold tokens and at L2 doc   */
+                             /*    windows, heavy first, rebuilt every iteration from the   */
+                             /*    flagged runs (items without one never reach the sampler) */
+                             /* 1: the same static list, every item staged every iteration  */
+                             /* 2: no balancing: one item per word, in word order (ablation)*/
+                             /* Performance only: the topics do not depend on it.           */
 } ezlda_options;
 
 /* debug_flags bits.  NO_TAIL_ROWS: word-prep precomputes the fixed-point rows of the dense

@@ -269,6 +269,13 @@ struct ezlda {
   uint32_t exact_all = 0;             // options.exact_draws
   uint32_t branches = 3;              // options.sampler (2: two-branch ESCA mode)
   uint32_t debug_flags = 0;           // options.debug_flags (EZLDA_DEBUG_*)
+  uint32_t schedule = 0;              // options.schedule
+  // H4 per-iteration schedule: CUB select of the live items (static order preserved)
+  uint32_t* item_iota = nullptr;
+  uint32_t* item_act = nullptr;
+  uint32_t* n_act = nullptr;
+  void* sel_tmp = nullptr;
+  size_t sel_tmp_bytes = 0;
   ezlda_iter_stats sum{};
   uint32_t sum_n = 0;
   double* llpt_partial = nullptr;
@@ -517,6 +524,7 @@ void fill_dev(ezlda* h) {
   d.rs = ezl::wrow_stride(h->K);
   ezl::seg_config(h->K, &d.segw, &d.segsub, &d.segfb);
   d.dt = ezl::d_shift(h->K);
+  d.grp = ezl::sampler_group_runs(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
   d.c1_cap = (h->debug_flags & EZLDA_DEBUG_C1_LOOKUP) ? 0u : 0x7FFFu;
   {
@@ -745,14 +753,14 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   st = cub_call(h, [&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, len32, tokpre, (int)(R + 1), s); });
   if (st) return st;
   h->release(len32);
-  const uint32_t split = o.split_threshold ? o.split_threshold : 10000u;
+  const uint32_t split = (o.schedule == 2) ? 0xFFFFFFFFu : (o.split_threshold ? o.split_threshold : 10000u);
   EZ_ALLOC(h, ihead, uint32_t, R);
   // L2 doc windows of doc_block_kb KiB of D rows (0 = 32 MiB): the items of hot words (at
   // least EZLDA_WIN_TOK tokens per window on average) are cut at window boundaries and run
   // window-major, heavy first -- every D row of the window is then read by many items
   // while it is L2 resident; the other words' items (too few runs per window to amortise
   // the staged What' row) run uncut after them
-  const uint64_t blk_kb = o.doc_block_kb ? o.doc_block_kb : 32768ull;
+  const uint64_t blk_kb = (o.schedule == 2) ? 0xFFFFFFFFull : (o.doc_block_kb ? o.doc_block_kb : 32768ull);
   const uint32_t blk_words = (uint32_t)std::min<uint64_t>(blk_kb * 256ull, 0xFFFFFFFFull);
   const uint64_t nwin = (h->Dwords + blk_words - 1) / blk_words;
 #ifndef EZLDA_WIN_TOK
@@ -830,7 +838,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     const uint64_t blk = cold ? 0u : it5[5 * a + 4];
     return (cold << 63) | (blk << 32) | (uint64_t)(0xFFFFFFFFu - it5[5 * a + 3]);
   };
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+  if (o.schedule != 2)  // schedule 2 (ablation): items stay in word order
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
   std::vector<uint32_t> iw(NI), ir0(NI), ir1(NI), int_(NI);
   for (uint32_t i = 0; i < NI; ++i) {
     const uint32_t q = order[i];
@@ -880,6 +889,19 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   d.item_r0 = item_r0;
   d.item_r1 = item_r1;
   d.item_ntok = item_ntok;
+  if (h->schedule == 0 && h->branches == 3 && NI) {  // H4: per-iteration list of the live items
+    EZ_ALLOC(h, h->item_iota, uint32_t, NI);
+    EZ_ALLOC(h, h->item_act, uint32_t, NI);
+    EZ_ALLOC(h, h->n_act, uint32_t, 1);
+    EZ_ALLOC(h, d.item_live, uint8_t, NI);
+    k_iota<<<blocks(NI), 256, 0, s>>>(h->item_iota, NI);
+    h->sel_tmp_bytes = 0;
+    EZ_CUDA(h, cub::DeviceSelect::Flagged(nullptr, h->sel_tmp_bytes, h->item_iota, d.item_live, h->item_act, h->n_act,
+                                          (int)NI, s));
+    EZ_ALLOC(h, h->sel_tmp, unsigned char, std::max<size_t>(h->sel_tmp_bytes, 1));
+    d.item_act = h->item_act;
+    d.n_act = h->n_act;
+  }
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
@@ -1050,6 +1072,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   if (o.w_mode > 2) return bad(EZLDA_E_INVALID, "unknown w_mode");
   if (o.sampler != 0 && o.sampler != 2 && o.sampler != 3)
     return bad(EZLDA_E_INVALID, "sampler must be 0/3 (three-branch) or 2 (two-branch)");
+  if (o.schedule > 2) return bad(EZLDA_E_INVALID, "schedule must be 0, 1 or 2");
   ezlda* h = new (std::nothrow) ezlda();
   if (!h) return bad(EZLDA_E_NOMEM, "host allocation failed");
   h->N = n_tokens;
@@ -1067,6 +1090,7 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
   h->exact_all = o.exact_draws ? 1u : 0u;
   h->branches = o.sampler ? o.sampler : 3u;
   h->debug_flags = o.debug_flags;
+  h->schedule = o.schedule;
   h->dev.token_base = o.token_base;
   ezlda_status st = EZLDA_OK;
   if (o.stream) {
@@ -1142,6 +1166,11 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
       ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
+      if (h->item_act) {  // H4: this iteration's live items (static heavy-first order kept)
+        ezl::launch_item_schedule(h->dev, nxt, h->n_items, s);
+        EZ_CUDA(h, cub::DeviceSelect::Flagged(h->sel_tmp, h->sel_tmp_bytes, h->item_iota, h->dev.item_live,
+                                              h->item_act, h->n_act, (int)h->n_items, s));
+      }
       ezl::launch_sampler(h->dev, cur, nxt, h->n_items, i, false, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
     }
@@ -1160,6 +1189,7 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     sl.launches = 3u + (h->n_docs_w ? 1u : 0u) + (h->n_docs_b ? 1u : 0u) - (h->n_items ? 0u : 1u);
     if (h->branches == 2) sl.launches = ezl::two_branch_word_major(h->K) ? sl.launches - 1u : sl.launches + 1u;
     if (h->multi && h->Vt) sl.launches += (h->R > h->rt0 ? 1u : 0u) + 1u;  // tail gather + tail rebuild
+    if (h->item_act && h->branches == 3) sl.launches += 2u;               // item schedule + CUB select
     h->pending.push_back(si);
     h->cur = 1 - h->cur;
     h->iteration = i;

@@ -1311,10 +1311,11 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
   uint32_t i = 0;
   if (lane == 0) i = (uint32_t)atomicAdd(&d.ctr->item_ctr, 1ull);
   i = __shfl_sync(kFull, i, 0);
-  if (i >= n_items) {
+  if (i >= (d.n_act ? *d.n_act : n_items)) {
     if (lane == 0) st_release_s(&c.state, k | kExit);
     return;
   }
+  if (d.item_act) i = d.item_act[i];  // this iteration's schedule (H4): items with a flagged run
   const uint32_t v = d.item_word[i];
   uint32_t* mrow = reinterpret_cast<uint32_t*>(sbase);
   const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&c.mbar);
@@ -1513,9 +1514,11 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     bool pf_ok = false;  // a claimed run group (pf_rb) whose flag words (pf_fw) are in flight
     uint32_t pf_rb = 0, pf_fw = 0;
     while (true) {
-      // refill the queue with flagged runs (warp-uniform control flow throughout); the
-      // next group of 32 runs is claimed and its flag words requested one refill ahead
-      while (qn < 32 && !exhausted) {
+      // refill the queue with flagged runs (warp-uniform control flow throughout): groups of
+      // G = d.grp runs are claimed from the item's cursor (G = 32, or fewer at large K so that
+      // an item's long rows spread over more warps), the next group one refill ahead
+      const uint32_t G = d.grp;
+      while (qn < G && !exhausted) {
         uint32_t rb, fw;
         if (pf_ok) {
           rb = pf_rb;
@@ -1524,15 +1527,15 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         } else {
           uint32_t grp = 0;
           if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
-          rb = r0 + __shfl_sync(kFull, grp, 0) * 32u;
-          fw = (rb + lane < r1) ? d.flags[(rb + lane) >> 5] : 0u;
+          rb = r0 + __shfl_sync(kFull, grp, 0) * G;
+          fw = (lane < G && rb + lane < r1) ? d.flags[(rb + lane) >> 5] : 0u;
         }
         if (rb >= r1) {
           exhausted = true;
           break;
         }
         const uint32_t r = rb + lane;
-        const bool act = (r < r1) && ((fw >> (r & 31u)) & 1u);
+        const bool act = lane < G && (r < r1) && ((fw >> (r & 31u)) & 1u);
         const uint32_t m = __ballot_sync(kFull, act);
         if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
         qn += __popc(m);
@@ -1542,8 +1545,8 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
       if (!exhausted && !pf_ok) {
         uint32_t grp = 0;
         if (lane == 0) grp = atomicAdd(&c.cursor, 1u);
-        pf_rb = r0 + __shfl_sync(kFull, grp, 0) * 32u;
-        pf_fw = (pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
+        pf_rb = r0 + __shfl_sync(kFull, grp, 0) * G;
+        pf_fw = (lane < G && pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
       uint32_t nb = sample_batch<kSegW, kSub, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, &c.qp, hist, ws,
@@ -1650,6 +1653,38 @@ __global__ void __launch_bounds__(256) k_tail_rebuild(Dev d, Buf nxt, const uint
   __syncthreads();
   const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, &s_run, 16u);
   if (threadIdx.x == 0) nxt.tnnz[t] = nz;
+}
+
+// H4 per iteration: warp per item, flagged runs of the item counted from the flag bitset.
+// An item without a flagged run holds only skipped tokens (z^i = K1 for all of them): its W
+// row / n_k contribution is written here and the sampler never stages it.
+__global__ void __launch_bounds__(256) k_item_schedule(Dev d, Buf nxt, uint32_t n_items) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t item = blockIdx.x * 8u + (threadIdx.x >> 5);
+  if (item >= n_items) return;
+  const uint32_t r0 = d.item_r0[item], r1 = d.item_r1[item];
+  uint32_t f = 0;
+  const uint32_t w0 = r0 >> 5, w1 = (r1 - 1u) >> 5;
+  for (uint32_t wb = w0 + lane; wb <= w1; wb += 32u) {
+    uint32_t x = d.flags[wb];
+    if (wb == w0) x &= 0xFFFFFFFFu << (r0 & 31u);
+    if (wb == w1 && (r1 & 31u) != 0u) x &= 0xFFFFFFFFu >> (32u - (r1 & 31u));
+    f |= x;
+  }
+  const uint32_t any = __any_sync(kFull, f != 0u) ? 1u : 0u;
+  if (lane == 0) {
+    d.item_live[item] = (uint8_t)any;
+    if (!any) {
+      const uint32_t v = d.item_word[item], n = d.item_ntok[item], K1 = d.rec[v].K[0];
+      if (v < d.Vd) {
+        atomicAdd(&nxt.Wd[(size_t)v * d.K + K1], (int32_t)n);
+      } else {  // a tail word has exactly one item: its row is the single entry (K1, n)
+        nxt.Wt[d.tofs[v - d.Vd]] = (K1 << 16) | n;
+        nxt.tnnz[v - d.Vd] = 1u;
+      }
+      atomicAdd(&nxt.nk[K1], (int32_t)n);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -1907,6 +1942,11 @@ void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb) {
   while (w * kSegCap < K) w <<= 1;
   *fb = w;
 }
+#ifndef EZLDA_GRP_LARGEK
+#define EZLDA_GRP_LARGEK 32  // runs per work claim when K > 4096 (A/B: 8, 16, 32)
+#endif
+uint32_t sampler_group_runs(uint32_t K) { return K <= kSegCap * 16u ? 32u : (uint32_t)EZLDA_GRP_LARGEK; }
+
 constexpr size_t kMaxSmem = 227u * 1024u;
 // shared-memory layout of the sampler block: kMaxSlots SlotCtl | nslots x (slot head [+ hist])
 // | kSampWarpsP x warp scratch.  kMaxSlots (3) slots with the histograms and the Q' table in
@@ -2064,6 +2104,10 @@ void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_ite
       void* args[] = {(void*)&d, (void*)&cur, (void*)&nxt, (void*)&iteration, (void*)&n_items};
       cudaLaunchKernel(ks, dim3(grid), dim3(kSampWarpsP * 32), args, sampler_smem_bytes(d.K), s);
     }
+}
+
+void launch_item_schedule(const Dev& d, const Buf& nxt, uint32_t n_items, cudaStream_t s) {
+  if (n_items) k_item_schedule<<<(n_items + 7) / 8, 256, 0, s>>>(d, nxt, n_items);
 }
 
 void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,

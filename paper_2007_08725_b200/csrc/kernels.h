@@ -76,6 +76,7 @@ struct Dev {
   uint32_t segsub;  // entries per S' checkpoint chunk (8: one per sector; or segw)
   uint32_t segfb;   // fallback segment width for runs longer than kSegCap x segw (0: none)
   uint32_t dt;      // topic shift of the packed D entries (d_shift(K))
+  uint32_t grp;     // runs per sampler work claim (32; smaller at large K, sampler_group_runs)
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
   // static structure
@@ -92,6 +93,11 @@ struct Dev {
   const uint32_t* item_r0;
   const uint32_t* item_r1;
   const uint32_t* item_ntok;
+  // per-iteration schedule (H4): the items holding a flagged run, in the static heavy-first
+  // order (item_act[0 .. *n_act)); nullptr = every item
+  const uint32_t* item_act;
+  const uint32_t* n_act;
+  uint8_t* item_live;  // [items] 1 iff the item has a flagged run (k_item_schedule)
   // dynamic state
   uint32_t* D;
   uint32_t* flags;
@@ -120,6 +126,9 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
 // sampler over items; count_only=true rebuilds W/n_k of `cur.z` into `nxt` (init, set_topics)
 void launch_sampler(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
                     bool count_only, cudaStream_t s);
+// H4: mark the items with a flagged run (item_live) and write the W / n_k contribution of the
+// others (every token skipped, so all of them stay at K1) into nxt
+void launch_item_schedule(const Dev& d, const Buf& nxt, uint32_t n_items, cudaStream_t s);
 // two-branch (ESCA) mode: What rows + Q prefixes of every word, then one draw per token
 // (D rows already rebuilt from cur.z) into nxt.z
 // (and W / n_k of the new topics into nxt).  K small enough for the word's tables in shared
@@ -151,6 +160,7 @@ SamplerLayout sampler_layout(uint32_t K);
 uint32_t sampler_qp_scratch_stride(uint32_t Kpad);  // doubles per slot of qp_scratch
 uint32_t wrow_stride(uint32_t K);
 void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb);
+uint32_t sampler_group_runs(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);
 // Raise the dynamic shared-memory limits of the kernels K needs (never lowered: handles with
 // different K may be alive at once) and return this K's persistent sampler grid in *grid.

@@ -30,7 +30,7 @@ class Options(C.Structure):
         ("nccl_unique_id", C.c_void_p), ("token_base", C.c_uint64), ("stream", C.c_void_p),
         ("input_on_device", C.c_uint32), ("no_phase_timing", C.c_uint32), ("doc_block_kb", C.c_uint32),
         ("exact_draws", C.c_uint32), ("sampler", C.c_uint32), ("local_group", C.c_uint64),
-        ("debug_flags", C.c_uint32),
+        ("debug_flags", C.c_uint32), ("schedule", C.c_uint32),
     ]
 
 
@@ -117,7 +117,7 @@ class EzLDA:
                  dense_threshold: int = 0, split_threshold: int = 0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, token_base: int = 0, stream: int | None = None,
                  phase_timing: bool = True, doc_block_kb: int = 0, exact_draws: bool = False,
-                 local_group: int = 0, sampler: int = 3, debug_flags: int = 0):
+                 local_group: int = 0, sampler: int = 3, debug_flags: int = 0, schedule: int = 0):
         L = load()
         self._h = None
         on_dev = bool(getattr(word_ids, "is_cuda", False))
@@ -143,6 +143,7 @@ class EzLDA:
         o.local_group = local_group
         o.sampler = sampler  # 3: three-branch (default), 2: two-branch ESCA baseline mode
         o.debug_flags = debug_flags  # EZLDA_DEBUG_* test hooks (rarely taken paths; same topics)
+        o.schedule = schedule  # 0 per-iteration active items, 1 static list, 2 no balancing (ablation)
         h = C.c_void_p()
         rc = L.ezlda_create(_addr(word_ids), _addr(doc_ids), self.N, self.n_docs, self.V, self.K, self.alpha,
                             self.beta, seed, C.byref(o), C.byref(h))

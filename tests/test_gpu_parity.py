@@ -239,7 +239,7 @@ def test_appendix_a_state_loglik(ez):
 @pytest.mark.parametrize("knobs", [
     dict(w_mode=1), dict(w_mode=2), dict(dense_threshold=3), dict(split_threshold=64),
     dict(split_threshold=64, w_mode=1), dict(g=1), dict(g=3), dict(doc_block_kb=1),
-    dict(doc_block_kb=1, split_threshold=100),
+    dict(doc_block_kb=1, split_threshold=100), dict(schedule=1), dict(schedule=2),
 ])
 def test_knob_invariance(ez, oracle_mod, tiny, knobs):
     """Dense threshold, W mode, region split, doc windows and g change speed only: T
