@@ -1943,7 +1943,7 @@ void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb) {
   *fb = w;
 }
 #ifndef EZLDA_GRP_LARGEK
-#define EZLDA_GRP_LARGEK 32  // runs per work claim when K > 4096 (A/B: 8, 16, 32)
+#define EZLDA_GRP_LARGEK 16  // runs per work claim when K > 4096 (A/B at NYTimes K=5k/10k: 8 55.2/91.7, 16 53.0/90.7, 32 53.9/93.8 ms)
 #endif
 uint32_t sampler_group_runs(uint32_t K) { return K <= kSegCap * 16u ? 32u : (uint32_t)EZLDA_GRP_LARGEK; }
 
