@@ -154,6 +154,7 @@ def arm_config(cfg, args, world: int) -> dict:
             "g": args.g, "w_mode": args.w_mode, "split_threshold": args.split or 10000,
             "exact_draws": bool(args.exact_draws), "doc_block_kb": args.doc_block_kb or 32768,
             "sampler": "two-branch (ESCA)" if args.sampler == 2 else "three-branch",
+            "schedule": ["per-iteration live items", "static item list", "no balancing"][args.schedule],
             "iterations_timed": [args.warmup + 1, args.warmup + args.steps],
             "parallelism": f"doc-partitioned x{world}",
             "l2": "inputs exceed L2 (corpus state "
@@ -220,6 +221,8 @@ def main():
     ap.add_argument("--g", type=int, default=2, help="S_est depth g in {1,2,3} (Eq 10)")
     ap.add_argument("--split", type=int, default=0, help="large-word region size in tokens (0 = 10000)")
     ap.add_argument("--exact-draws", action="store_true", help="every sampled token on the exact fp64 path")
+    ap.add_argument("--schedule", type=int, default=0, choices=[0, 1, 2],
+                    help="sampler schedule: 0 per-iteration live items (default), 1 static list, 2 no balancing")
     ap.add_argument("--sampler", type=int, default=3, choices=[2, 3],
                     help="3: three-branch (default); 2: the paper's two-branch ESCA baseline mode (NEXT-1)")
     ap.add_argument("--ncu-traffic", default=os.path.join(ROOT, "profiles", "ncu_traffic.json"))
@@ -270,7 +273,7 @@ def main():
     torch.cuda.set_stream(stream)
     t_create = time.perf_counter()
     knobs = dict(doc_block_kb=args.doc_block_kb, w_mode=args.w_mode, g=args.g, split_threshold=args.split,
-                 exact_draws=args.exact_draws, sampler=args.sampler)
+                 exact_draws=args.exact_draws, sampler=args.sampler, schedule=args.schedule)
     ez = lda.EzLDA(w, d, doc_hi - doc_lo, cfg.V, cfg.K, seed=SAMPLER_SEED, rank=rank, world=world,
                    nccl_id=nccl_id, token_base=t0, stream=stream.cuda_stream, **knobs)
     torch.cuda.synchronize()
