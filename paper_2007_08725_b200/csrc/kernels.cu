@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <vector>
 
 #include "kernels.h"
 
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
     r.a[i] = ok ? bv : 0.0;
     r.K[i] = ok ? (uint16_t)bk : (uint16_t)0;
   }
+  __syncwarp();  // every lane's reads of the row (top-4 scan) precede lane 0's write below
   if (lane == 0) row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
   __syncwarp();
   const bool out = v < d.Vw;
@@ -472,7 +474,11 @@ __device__ __forceinline__ void mpt_token(const Dev& d, const Buf& nxt, uint32_t
   const uint32_t C3 = d.geff >= 3 ? C(r.K[2]) : 0u;
   const double M = mpt_M(r, C1, d.alpha);
   const double den = mpt_den(r, M, C1, C2, C3, L, d.geff);
+#ifdef EZLDA_EXP_DOC_NOPHILOX  // diagnostic: a cheap hash instead of Philox in the doc pass
+  const double u = (double)((j * 2654435761u) >> 8) * 0x1p-24;
+#else
   const double u = philox_u(d.seed, iter, d.token_base + j);
+#endif
   if (mpt_skip(u, M, den)) {
     nxt.z[j] = r.K[0];
     ++n_skip;
@@ -770,16 +776,51 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
 //                        is certified against the fixed-point error bound or the token is
 //                        redrawn by exact_draw with the oracle's fp64 operations, so the
 //                        topics equal the oracle's.
+#ifdef EZLDA_EXP_FAKEROW
+__device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over [0, 1000)
+#endif
+#ifndef EZLDA_SCAN_DYN
+#define EZLDA_SCAN_DYN 1
+#endif
+#ifndef EZLDA_B_PF
+#define EZLDA_B_PF 1
+#endif
+#ifndef EZLDA_SEGW_SMALL
+#define EZLDA_SEGW_SMALL 16u  // S' segment width when K <= kSegCap x 16 (16 or 32 entries per lane and round)
+#endif
 struct RunCounters {
   uint32_t sampled, hitM, runs, words, exact;
 };
 
 constexpr int kQueue = 64;  // one batch + one refill group
 
-struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | queue
-  unsigned long long* P;  // fixed-point prefix checkpoints of the batch's runs (see sample_batch)
-  uint32_t* q;            // queue of flagged runs
+struct WarpScratch {  // per-warp shared memory (d.ws_bytes): checkpoints | queue (32-bit shared addresses)
+  uint32_t P;     // u64 fixed-point prefix checkpoints of the batch's runs (see sample_batch)
+  uint32_t q;     // ring of kQueue flagged runs
+  uint32_t head;  // ring position of the queue's first entry
 };
+__device__ __forceinline__ unsigned long long lds_u64(uint32_t addr) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u64x2(uint32_t addr, unsigned long long a, unsigned long long b) {
+  asm volatile("st.shared.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void sts_u64(uint32_t addr, unsigned long long a) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(addr), "l"(a) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32v(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t a) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
+}
+__device__ __forceinline__ uint32_t ws_q_at(const WarpScratch& ws, uint32_t i) {
+  return ws.q + 4u * ((ws.head + i) & (uint32_t)(kQueue - 1));
+}
 
 // 32-byte (one sector) read-only load
 __device__ __forceinline__ void ldg256(const uint32_t* p, uint4& a, uint4& b) {
@@ -801,6 +842,9 @@ template <uint32_t kDTs>
 __device__ __forceinline__ unsigned long long entry_mac(uint32_t w, uint32_t row_s, unsigned long long acc) {
   // dt = 18: w >> 16 = 4 topic (one LEA.HI); dt = 16: 4 topic = (w >> 14) & ~3
   const uint32_t off = (kDTs == 18u) ? (w >> 16) : ((w >> 14) & ~3u);
+#ifdef EZLDA_EXP_NOCONFLICT  // diagnostic: every lane gathers one address (no bank conflicts)
+  return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + (off & 4u));
+#endif
   return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + off);
 }
 
@@ -945,7 +989,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   const uint32_t nc = min(qn, 32u);
   uint32_t j0 = 0, ebase = 0, len = 0, nnz = 0, nseg = 0, Ld = 0;
   if (lane < nc) {
-    const uint32_t r = ws.q[lane];
+    const uint32_t r = lds_u32v(ws_q_at(ws, lane));
     j0 = d.run_j0[r];
     const uint32_t dbase = d.run_dbase[r];
     len = d.run_len[r];
@@ -969,6 +1013,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   if (nb == 0) return 0;  // the first run alone exceeds a batch: the caller takes its wide-segment path
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
   const uint32_t soff = sincl - nseg;
+#if EZLDA_SCAN_DYN
+  // the segmented scan of phase B needs offsets below the longest admitted run (<= 32 lanes)
+  const uint32_t smax = __reduce_max_sync(kFull, lane < nb ? nseg : 0u);
+#else
+  const uint32_t smax = 32u;
+#endif
   tincl = (lane < nb) ? len : 0u;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1001,18 +1051,53 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   //      fixed-point What' row), combined by a segmented warp scan (+ carry across rounds).
   //      Checkpoints: P[kCk g + i] = P(before g) + (chunks 0..i of g); the last one is
   //      P(end of g), and S' = the run's last checkpoint.
-  static_assert(kCk == 1u || kCk == 2u, "checkpoints per segment");
+  static_assert(kCk == 1u || kCk == 2u || kCk == 4u, "checkpoints per segment");
   unsigned long long carry = 0ull;
-  for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
+#if EZLDA_B_PF
+  // software pipeline (kSegW == 16): the two sectors of round B0 + 32 are requested before
+  // round B0 is accumulated, so a warp keeps two rounds of D-row loads in flight
+  constexpr bool kPf = (kSegW == 16u);
+#else
+  constexpr bool kPf = false;
+#endif
+  uint4 fa = make_uint4(0u, 0u, 0u, 0u), fb = fa, fc = fa, fd = fa;  // prefetched round (kPf)
+  uint32_t f_soff = 0;
+  auto round_load = [&](uint32_t B0, uint32_t& o_soff, uint4& qa, uint4& qb, uint4& qc, uint4& qd) {
     const uint32_t g = B0 + lane;
     const uint32_t slot = slot_of(B0, soff);
-    const uint32_t s_soff = __shfl_sync(kFull, soff, slot);
+    o_soff = __shfl_sync(kFull, soff, slot);
+    const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
+    const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
+    const uint32_t e0 = (g - o_soff) * 16u;
+    const uint32_t* p = d.D + s_ebase + e0;
+    qa = qb = qc = qd = make_uint4(0u, 0u, 0u, 0u);
+    if (g < T && e0 < s_nnz) ldg256(p, qa, qb);
+    if (g < T && e0 + 8u < s_nnz) ldg256(p + 8u, qc, qd);
+  };
+  if (kPf) round_load(0u, f_soff, fa, fb, fc, fd);
+  for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
+    const uint32_t g = B0 + lane;
+    unsigned long long acc = 0ull;
+    unsigned long long part[4] = {0ull, 0ull, 0ull, 0ull};  // running sums after each sector (kSub == 8)
+    uint32_t s_soff;
+    if (kPf) {
+      const uint4 ca = fa, cb = fb, cc = fc, cd = fd;
+      s_soff = f_soff;
+      if (B0 + 32u < T) round_load(B0 + 32u, f_soff, fa, fb, fc, fd);
+      acc = sector_mac<kDTs>(acc, ca, cb, row_s);
+      part[0] = acc;
+      acc = sector_mac<kDTs>(acc, cc, cd, row_s);
+    } else {
+    const uint32_t slot = slot_of(B0, soff);
+    s_soff = __shfl_sync(kFull, soff, slot);
     const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
     const uint32_t e0 = (g - s_soff) * kSegW;
+#ifdef EZLDA_EXP_FAKEROW  // diagnostic: D-row memory traffic removed (entries from a 4 KB table)
+    const uint32_t* p = g_fake + ((s_ebase + e0) & 0x3F0u);
+#else
     const uint32_t* p = d.D + s_ebase + e0;
-    unsigned long long acc = 0ull;
-    unsigned long long part[1] = {0ull};  // running sum after the first sector (kCk == 2)
+#endif
     if (g < T) {
       {
 #pragma unroll(kSegW <= 64u ? 4 : 2)
@@ -1021,30 +1106,42 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           if (e0 + b < s_nnz) ldg256(p + b, qa, qb);
           if (e0 + b + 8u < s_nnz) ldg256(p + b + 8u, qc, qd);
           acc = sector_mac<kDTs>(acc, qa, qb, row_s);
-          if (kCk == 2u) part[0] = acc;
+          if (kSub == 8u) part[(b >> 3) & 3u] = acc;
           acc = sector_mac<kDTs>(acc, qc, qd, row_s);
+          if (kSub == 8u) part[((b >> 3) + 1u) & 3u] = acc;
         }
       }
+    }
     }
     const unsigned long long tot = acc;
     // segmented inclusive scan over the lanes of one run (lanes >= rs belong to it)
     const uint32_t rs = (s_soff > B0) ? s_soff - B0 : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
+      if ((uint32_t)o >= smax) break;
       const unsigned long long y = __shfl_up_sync(kFull, acc, o);
       if (lane >= rs + (uint32_t)o) acc += y;
     }
     if (s_soff < B0) acc += carry;  // the run started in an earlier round
     if (g < T) {
       if (kCk == 1u) {
-        ws.P[g] = acc;
-      } else {
+        sts_u64(ws.P + 8u * g, acc);
+      } else if (kCk == 2u) {
         const unsigned long long excl = acc - tot;  // prefix before segment g
-        // kCk == 2: the two checkpoints of a segment are adjacent: one 16-byte store
+        // the two checkpoints of a segment are adjacent: one 16-byte store
         ulonglong2 pr;
         pr.x = excl + part[0];
         pr.y = acc;
-        *reinterpret_cast<ulonglong2*>(ws.P + 2u * g) = pr;
+        sts_u64x2(ws.P + 16u * g, pr.x, pr.y);
+      } else {
+        const unsigned long long excl = acc - tot;
+        ulonglong2 p0, p1;
+        p0.x = excl + part[0];
+        p0.y = excl + part[1];
+        p1.x = excl + part[2];
+        p1.y = acc;
+        sts_u64x2(ws.P + 32u * g, p0.x, p0.y);
+        sts_u64x2(ws.P + 32u * g + 16u, p1.x, p1.y);
       }
     }
     carry = __shfl_sync(kFull, acc, 31);
@@ -1079,7 +1176,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       C1 = row_count(d, E, s_nnz, K1);
     }
     const uint32_t c0 = kCk * s_soff, nck = kCk * s_nseg;
-    const unsigned long long Spi = nck ? ws.P[c0 + nck - 1u] : 0ull;
+    const unsigned long long Spi = nck ? lds_u64(ws.P + 8u * (c0 + nck - 1u)) : 0ull;
     const double Sp = (double)Spi * inv_s;  // exact: Spi < 2^48
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
@@ -1104,13 +1201,17 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
         uint32_t a = c0, b = c0 + nck - 1u;
         while (a < b) {
           const uint32_t mid = (a + b) >> 1;
-          if (ws.P[mid] > Yf) b = mid; else a = mid + 1u;
+          if (lds_u64(ws.P + 8u * mid) > Yf) b = mid; else a = mid + 1u;
         }
-        const unsigned long long base = (a > c0) ? ws.P[a - 1u] : 0ull;
+        const unsigned long long base = (a > c0) ? lds_u64(ws.P + 8u * (a - 1u)) : 0ull;
         unsigned long long pb = base, pa = base;  // prefixes before / after the candidate
         if (kSub == 8u) {  // one sector (8 entries; zero padding past nnz) from registers
           uint4 qa, qb;
+#ifdef EZLDA_EXP_FAKEROW
+          ldg256(g_fake + ((s_ebase + 16u * ((a - c0) >> 1)) & 0x3F0u) + 8u * ((a - c0) & 1u), qa, qb);
+#else
           ldg256(E + (a - c0) * 8u, qa, qb);
+#endif
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -1460,8 +1561,9 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
   WarpScratch ws;
   {
     unsigned char* wb = slots + nsl * sb + warp * d.ws_bytes;
-    ws.P = reinterpret_cast<unsigned long long*>(wb);
-    ws.q = reinterpret_cast<uint32_t*>(wb + d.ws_bytes - 4u * kQueue);
+    ws.P = (uint32_t)__cvta_generic_to_shared(wb);
+    ws.q = ws.P + d.ws_bytes - 4u * kQueue;
+    ws.head = 0;
   }
   // histogram of slot sl: shared memory after the slot head, or this block's HBM scratch
   auto hist_of = [&](uint32_t sl) -> uint32_t* {
@@ -1498,6 +1600,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
       while (((st = ld_acquire_s(&c.state)) & ~kExit) != k) __nanosleep(32);
     }
     st = __shfl_sync(kFull, st, 0);
+    __syncwarp();  // orders lane 0's acquire before the other lanes' reads of the slot
     if (st & kExit) break;
     mbar_wait((uint32_t)__cvta_generic_to_shared(&c.mbar), (k / nsl) & 1u);
     // fixed-point Q' table: in the slot right after the scales, or in HBM (kQG, large K)
@@ -1537,7 +1640,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         const uint32_t r = rb + lane;
         const bool act = lane < G && (r < r1) && ((fw >> (r & 31u)) & 1u);
         const uint32_t m = __ballot_sync(kFull, act);
-        if (act) ws.q[qn + __popc(m & lanemask_lt())] = r;
+        if (act) sts_u32(ws_q_at(ws, qn + __popc(m & lanemask_lt())), r);
         qn += __popc(m);
         __syncwarp();
       }
@@ -1555,12 +1658,8 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         nb = sample_batch<kFbW ? kFbW : 16u, kFbW ? kFbW : 16u, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl,
                                                                           &c.qp, hist, ws, qn, iter, rc);
 
-      // drop the processed runs from the queue
-      const uint32_t keep0 = (lane + nb < qn) ? ws.q[lane + nb] : 0u;
-      const uint32_t keep1 = (lane + 32u + nb < qn) ? ws.q[lane + 32u + nb] : 0u;
-      __syncwarp();
-      if (lane + nb < qn) ws.q[lane] = keep0;
-      if (lane + 32u + nb < qn) ws.q[lane + 32u] = keep1;
+      // drop the processed runs from the queue (ring)
+      ws.head += nb;
       qn -= nb;
       __syncwarp();
     }
@@ -1933,6 +2032,7 @@ uint32_t wrow_stride(uint32_t K) {  // m | scales | qfx | ce | QP (doubles)
 void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb) {
   *segw = 16u;
   if (K <= kSegCap * 16u) {
+    *segw = EZLDA_SEGW_SMALL;
     *sub = 8u;
     *fb = 0u;
     return;
@@ -2001,7 +2101,9 @@ static const void* sampler_kernel_fb(uint32_t qg) {
 static const void* sampler_kernel(uint32_t K, uint32_t qg) {
   uint32_t segw, sub, fb;
   seg_config(K, &segw, &sub, &fb);
-  if (fb == 0u) return qg ? (const void*)k_sampler<16u, 8u, 0u, kDTSmall, true> : (const void*)k_sampler<16u, 8u, 0u, kDTSmall, false>;
+  if (fb == 0u)
+    return qg ? (const void*)k_sampler<EZLDA_SEGW_SMALL, 8u, 0u, kDTSmall, true>
+              : (const void*)k_sampler<EZLDA_SEGW_SMALL, 8u, 0u, kDTSmall, false>;
   switch (fb) {  // K > 4096: fallback segment width 32 .. 256 (K <= 65535)
     case 32u: return sampler_kernel_fb<32u, kDTSmall>(qg);
     case 64u: return sampler_kernel_fb<64u, kDTSmall>(qg);
@@ -2030,6 +2132,15 @@ static cudaError_t raise_smem(int dev, const void* k, int bytes) {
 cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   std::lock_guard<std::mutex> lk(g_attr_m);
   cudaError_t e;
+#ifdef EZLDA_EXP_FAKEROW
+  {
+    std::vector<uint32_t> f(1040);
+    for (uint32_t i = 0; i < 1040; ++i) f[i] = ((((i * 37u) % 61u) + 16u * (i % 16u)) % K) << 18 | 1u;
+    for (uint32_t i = 0; i < 1040; i += 16)  // ascending topics within each 16-entry segment
+      std::sort(f.begin() + i, f.begin() + std::min<uint32_t>(i + 16, 1040));
+    if ((e = cudaMemcpyToSymbol(g_fake, f.data(), 4 * f.size()))) return e;
+  }
+#endif
   int dev = 0, nsm = 0, nb = 0;
   if ((e = cudaGetDevice(&dev))) return e;
   if (K <= kWpSmallK && (e = raise_smem(dev, (const void*)k_word_prep_w, (int)word_prep_smem_bytes(K)))) return e;

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+export PYTHONUNBUFFERED=1
+for v in s16 s32 s16pf; do
+  EZLDA_LIB=$PWD/_variants/lib_$v.so timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "tiny or small or long_docs or rare_paths" 2>&1 | tail -1
+done
+STEPS=8 WARMUP=3 EXTRA="--curve-iters 0" bash tools/variants.sh "pubmed nytimes" $PWD/_variants/lib_base.so $PWD/_variants/lib_s16nodyn.so $PWD/_variants/lib_s16.so $PWD/_variants/lib_s32.so $PWD/_variants/lib_s16pf.so
