@@ -149,6 +149,8 @@ typedef struct {
   double exchange_bytes;     /* H7 collective payload of the iteration (world > 1): int32 all-  */
                              /* reduce of the dense W block + n_k, u16 all-gather of the tail  */
                              /* topics (output size); 0 when world == 1                        */
+  double ms_sampler_kernel;  /* the k_sampler launch alone (inside ms_sample, which also holds  */
+                             /* the H4 item schedule and the n_k column sums)                   */
 } ezlda_iter_stats;
 
 /* Build the resident corpus and draw z^0 (iteration 0).

@@ -258,7 +258,7 @@ struct ezlda {
   // per-iteration records (events + pinned counter copies), folded lazily into stats
   static constexpr int kSlots = 256;
   struct Slot {
-    cudaEvent_t ev[5];
+    cudaEvent_t ev[7];  // start | word records | doc pass | schedule | heads | sampler | end
     uint32_t iteration;
     uint32_t launches;
   };
@@ -521,7 +521,6 @@ void fill_dev(ezlda* h) {
   d.nch = (h->K + 31) / 32;
   d.Kpad = d.nch * 32;
   d.Vd = h->Vd;
-  d.rs = ezl::wrow_stride(h->K);
   ezl::seg_config(h->K, &d.segw, &d.segsub, &d.segfb);
   d.dt = ezl::d_shift(h->K);
   d.grp = ezl::sampler_group_runs(h->K);
@@ -556,8 +555,9 @@ ezlda_status rebuild_counts(ezlda* h) {
   EZ_CUDA(h, cudaGetLastError());
   ezlda_status s;
   if ((s = allreduce(h, b.Wd, (size_t)h->Vd * h->K, ncclInt32))) return s;
-  if ((s = allreduce(h, b.nk, h->K, ncclInt32))) return s;
   if ((s = merge_tail(h, b))) return s;
+  ezl::launch_nk(h->dev, b, h->stream);  // n_k of the global W (identical on every rank)
+  EZ_CUDA(h, cudaGetLastError());
   h->D_fresh = false;
   return EZLDA_OK;
 }
@@ -825,7 +825,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     EZ_ALLOC(h, h->tz_all, uint16_t, (size_t)h->world * h->tail_max);
     EZ_CUDA(h, cudaStreamSynchronize(s));
   }
-  if (h->multi) h->exchange_bytes = 4.0 * ((double)h->Vd * h->K + h->K) + 2.0 * h->world * (h->Vt ? h->tail_max : 0);
+  if (h->multi) h->exchange_bytes = 4.0 * (double)h->Vd * h->K + 2.0 * h->world * (h->Vt ? h->tail_max : 0);
   h->release(tokpre);
   h->release(wrun);
   // order: hot-word items window-major, heavy first within a window; then the other items
@@ -905,24 +905,27 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
-  // fixed-point What' | QP rows for every word when they fit in half of the free device
-  // memory, at most 64 GiB (the sampler then stages every item with one bulk copy), else for
-  // the dense words only (tail rows staged by a warp)
-  {
+  EZ_ALLOC(h, d.qexact, double, (size_t)h->V * d.nch);
+  // sampler heads (8 Kpad + 32 + ce bytes per word) for every word when they fit in half of
+  // the free device memory (at most 64 GiB), else for the dense words only (the other items
+  // are staged by a sampler warp)
+  d.rs_bytes = ezl::head_bytes(h->K);
+  if (h->branches == 3) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
     const uint64_t budget = std::min<uint64_t>(64ull << 30, fr / 2);
-    d.Vw = ((uint64_t)h->V * d.rs * 8ull <= budget) ? h->V : h->Vd;
+    d.Vw = ((uint64_t)h->V * d.rs_bytes <= budget) ? h->V : h->Vd;
     if (o.debug_flags & EZLDA_DEBUG_NO_TAIL_ROWS) d.Vw = h->Vd;  // tail rows staged by a sampler warp
-    if (h->branches == 2) d.Vw = 0;  // the two-branch mode does not use the three-branch records
   }
-  EZ_ALLOC(h, d.wrow, double, (size_t)d.Vw * d.rs);
+  EZ_ALLOC(h, d.wrow, unsigned char, (size_t)d.Vw * d.rs_bytes);
+  if (h->item_act) EZ_ALLOC(h, d.word_live, uint8_t, h->V);
   if (h->branches == 2 && !ezl::two_branch_word_major(h->K)) {
     EZ_ALLOC(h, d.tbw, double, (size_t)h->V * d.Kpad);
     EZ_ALLOC(h, d.tbq, double, (size_t)h->V * d.Kpad);
   }
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
+  EZ_ALLOC(h, d.inv_den, double, h->K);
   EZ_ALLOC(h, d.ctr, ezl::Counters, 1);
   for (int b = 0; b < 2; ++b) {
     Buf& B = h->buf[b];
@@ -945,13 +948,11 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(d_cnt);
   h->release(d_max);
   EZ_CUDA(h, ezl::configure_kernels(h->K, &d.sampler_grid));
-  {  // per-(sampler block, slot) scratch: HBM histograms (large K) and exact Q' tables of
-     // warp-staged tail rows
+  {  // per-(sampler block, slot) scratch: HBM histograms and fixed-point Q' tables (large K)
     const size_t nh = (size_t)d.sampler_grid * d.nslots * (d.Kpad + d.Kpad / 32);  // counts + bitmap
     EZ_ALLOC(h, d.hist_scratch, uint32_t, nh);
     EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
-    EZ_ALLOC(h, d.qp_scratch, double,
-             (size_t)d.sampler_grid * d.nslots * ezl::sampler_qp_scratch_stride(d.Kpad));
+    if (d.qfx_global) EZ_ALLOC(h, d.qfx_scratch, uint32_t, (size_t)d.sampler_grid * d.nslots * d.Kpad);
   }
   // ---- iteration 0
   h->cur = 0;
@@ -984,10 +985,16 @@ ezlda_status fold_one(ezlda* h) {
   st.exchange_bytes = h->exchange_bytes;
   if (h->timing) {
     float a = 0, b = 0, cc = 0, dd = 0;
+    float e25 = 0, e56 = 0, e63 = 0;
     EZ_CUDA(h, cudaEventElapsedTime(&a, sl.ev[0], sl.ev[1]));
     EZ_CUDA(h, cudaEventElapsedTime(&b, sl.ev[1], sl.ev[2]));
-    EZ_CUDA(h, cudaEventElapsedTime(&cc, sl.ev[2], sl.ev[3]));
+    EZ_CUDA(h, cudaEventElapsedTime(&e25, sl.ev[2], sl.ev[5]));
+    EZ_CUDA(h, cudaEventElapsedTime(&e56, sl.ev[5], sl.ev[6]));
+    EZ_CUDA(h, cudaEventElapsedTime(&e63, sl.ev[6], sl.ev[3]));
     EZ_CUDA(h, cudaEventElapsedTime(&dd, sl.ev[3], sl.ev[4]));
+    a += e56;           // word-prep = word records + the sampler heads of the live words
+    cc = e25 + e63;     // sampling = schedule + sampler + n_k
+    st.ms_sampler_kernel = e63;
     st.ms_wordprep = a;
     st.ms_docpass = b;
     st.ms_sample = cc;
@@ -1013,6 +1020,7 @@ ezlda_status fold_one(ezlda* h) {
   S.ms_wordprep += st.ms_wordprep;
   S.ms_docpass += st.ms_docpass;
   S.ms_sample += st.ms_sample;
+  S.ms_sampler_kernel += st.ms_sampler_kernel;
   S.ms_allreduce += st.ms_allreduce;
   S.n_tokens += st.n_tokens;
   S.skip_S += st.skip_S;
@@ -1159,7 +1167,10 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
       ezl::launch_doc_pass(h->dev, cur, cur, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, false, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[5], s));
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[6], s));
       ezl::launch_two_branch(h->dev, cur, nxt, h->n_items, i, s);
+      if (!h->multi) ezl::launch_nk(h->dev, nxt, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
     } else {
       ezl::launch_word_prep(h->dev, cur, s);
@@ -1167,11 +1178,16 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
       ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[2], s));
       if (h->item_act) {  // H4: this iteration's live items (static heavy-first order kept)
+        EZ_CUDA(h, cudaMemsetAsync(h->dev.word_live, 0, h->V, s));
         ezl::launch_item_schedule(h->dev, nxt, h->n_items, s);
         EZ_CUDA(h, cub::DeviceSelect::Flagged(h->sel_tmp, h->sel_tmp_bytes, h->item_iota, h->dev.item_live,
                                               h->item_act, h->n_act, (int)h->n_items, s));
       }
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[5], s));
+      ezl::launch_word_heads(h->dev, cur, s);  // heads of the live items' words (H1, second half)
+      if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[6], s));
       ezl::launch_sampler(h->dev, cur, nxt, h->n_items, i, false, s);
+      if (!h->multi) ezl::launch_nk(h->dev, nxt, s);  // H6: n_k column sums of the new W
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
     }
     EZ_CUDA(h, cudaGetLastError());
@@ -1179,8 +1195,9 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     // H7 (world > 1): int32 all-reduce of the dense block and n_k, all-gather of
     // the tail topics + tail-row rebuild (integer sums: W is identical on every rank)
     if ((st = allreduce(h, nxt.Wd, (size_t)h->Vd * h->K, ncclInt32))) return st;
-    if ((st = allreduce(h, nxt.nk, h->K, ncclInt32))) return st;
     if ((st = merge_tail(h, nxt))) return st;
+    if (h->multi) ezl::launch_nk(h->dev, nxt, s);  // n_k of the global W (identical on every rank)
+    EZ_CUDA(h, cudaGetLastError());
     EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaEventRecord(ev[4], s));
     sl.iteration = i;
@@ -1190,6 +1207,8 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     if (h->branches == 2) sl.launches = ezl::two_branch_word_major(h->K) ? sl.launches - 1u : sl.launches + 1u;
     if (h->multi && h->Vt) sl.launches += (h->R > h->rt0 ? 1u : 0u) + 1u;  // tail gather + tail rebuild
     if (h->item_act && h->branches == 3) sl.launches += 2u;               // item schedule + CUB select
+    sl.launches += 1u;                                                     // n_k column sums (k_nk)
+    if (h->branches == 3 && h->dev.Vw) sl.launches += 1u;                  // word heads
     h->pending.push_back(si);
     h->cur = 1 - h->cur;
     h->iteration = i;

@@ -157,36 +157,13 @@ __global__ void k_den(Dev d, Buf cur) {
     const double den = (double)cur.nk[k] + d.Vbeta;
     d.den[k] = den;
     d.what0[k] = d.beta / den;
+    d.inv_den[k] = 1.0 / den;  // sampler heads (stage_row_warp); the exact paths divide
   }
 }
 
-// wrow record of word v (u32 m | f64 scales {2^-s, 2^s, 2^-t, 2^t} | u32 qfx | f64 QP): the
-// head (m | scales, plus qfx unless d.qfx_global) is one bulk copy into a sampler slot; QP
-// (exact) stays in HBM for the exact redraws.
 // chunk ends of the fixed-point Q' table: ce[c] = qfx[32 c + 31] (contiguous, so the first
 // half of a Q' search probes one 128-byte line instead of one bank), padded to 16 bytes
 __host__ __device__ __forceinline__ uint32_t ce_words(uint32_t Kpad) { return ((Kpad / 32u) + 3u) & ~3u; }
-// per-slot HBM scratch of a warp-staged tail row, in doubles: QP f64 [Kpad] | qfx u32 [Kpad] | ce
-__host__ __device__ __forceinline__ uint32_t qp_scratch_stride(uint32_t Kpad) { return Kpad + Kpad / 2u + ce_words(Kpad) / 2u; }
-
-struct WrowPtrs {
-  uint32_t* m;
-  uint32_t* qfx;
-  uint32_t* ce;
-  double* sc;
-  double* qp;
-};
-__device__ __forceinline__ WrowPtrs wrow_ptrs(const Dev& d, uint32_t v) {
-  double* b = d.wrow + (size_t)v * d.rs;
-  WrowPtrs o;
-  o.m = reinterpret_cast<uint32_t*>(b);
-  o.sc = b + d.Kpad / 2u;
-  o.qfx = reinterpret_cast<uint32_t*>(o.sc + 4);
-  o.ce = o.qfx + d.Kpad;
-  o.qp = b + d.Kpad + 4u + ce_words(d.Kpad) / 2u;
-  return o;
-}
-
 // H1: word-prep, small K (K <= 4096).  One warp per word: stage the What row
 // in shared memory, top-4 (value desc, topic asc) by per-lane insertion + a 4-round warp
 // tournament, What' (K1 entry zeroed), then lane 0 runs the Q' prefix P_v(k) strictly
@@ -245,56 +222,31 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
   __syncwarp();  // every lane's reads of the row (top-4 scan) precede lane 0's write below
   if (lane == 0) row[r.K[0]] = 0.0;  // What' (Eq 6): the maximum entry set to 0
   __syncwarp();
-  const bool out = v < d.Vw;
-  WrowPtrs o = wrow_ptrs(d, v);
-  if (out) {  // fixed-point What'[v] (m = rint(What' 2^s), s from max What' = a2) + scale
-    int e = 0;
-    frexp(r.a[1], &e);
-    const int sh = 32 - e;  // max What' 2^sh in [2^31, 2^32)
-    for (uint32_t k = lane; k < d.Kpad; k += 32u)
-      o.m[k] = __double2uint_rn(fmin(ldexp(row[k], sh), 4294967295.0));
-    if (lane == 0) {
-      o.sc[0] = ldexp(1.0, -sh);
-      o.sc[1] = ldexp(1.0, sh);
-    }
-  }
-  double* outq = o.qp;
   if (lane == 0) {
-    // Q' prefix, strictly sequential; the next 8 entries are loaded before the dependent adds
+    // Q' = alpha sum_{k != K1} What[v][k], strictly sequential (the oracle's order, bit for
+    // bit); the next 8 entries are loaded before the dependent adds.  Every 32 topics the
+    // running sum is kept (qe: exact checkpoints of P_v for the sampler's exact redraws)
+    double* qe = d.qexact + (size_t)v * d.nch;
     double acc = 0.0, x[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = row[i];
-    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 8u) {  // Kpad is a multiple of 32
+    for (uint32_t k0 = 0; k0 < d.Kpad; k0 += 8u) {  // Kpad is a multiple of 32 (zero past K)
       double xn[8];
       const uint32_t kn = (k0 + 8u < d.Kpad) ? k0 + 8u : k0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) xn[i] = row[kn + i];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        acc = acc + x[i];
-        if (out) outq[k0 + i] = d.alpha * acc;
-        if (k0 + i == d.K - 1u) r.Qp = d.alpha * acc;
-      }
+      for (int i = 0; i < 8; ++i) acc = acc + x[i];
+      if ((k0 & 31u) == 24u) qe[k0 >> 5] = acc;  // exact P_v(32 c + 31), c = k0 / 32
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = xn[i];
     }
+    r.Qp = d.alpha * acc;
     d.rec[v] = r;
-    if (out) {
-      int e = 0;
-      frexp(r.Qp, &e);  // fixed-point Q' prefix: qfx = rint(QP 2^t), Q' 2^t in [2^31, 2^32)
-      o.sc[2] = ldexp(1.0, e - 32);
-      o.sc[3] = ldexp(1.0, 32 - e);
-    }
-  }
-  if (out) {
-    __syncwarp();
-    const double two_t = o.sc[3];
-    for (uint32_t k = lane; k < d.Kpad; k += 32u) o.qfx[k] = __double2uint_rn(fmin(outq[k] * two_t, 4294967295.0));
-    for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)
-      o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(outq[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
   }
 }
 
+// ---------------------------------------------------------------------------------
 // H1: word-prep, large K (K > 4096).  One warp per word, the What row in 256-topic chunks
 // staged in shared memory (2 KB per warp, so occupancy does not fall with K).  Pass 1: every
 // chunk filled with What[v][k] = (W[v][k] + beta) / den_k (dense rows; tail rows: the
@@ -350,15 +302,10 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
   // ---- pass 1: top-4 (value desc, topic asc) and an estimate of sum_k What
   Top4 t;
   top4_init(t);
-  double tot = 0.0;
   uint32_t tcur = 0;
   for (uint32_t c0 = 0; c0 < d.K; c0 += kWbChunk) {
     fill_what_chunk(d, cur, v, c0, ch, tcur);
-    for (uint32_t i = lane; i < kWbChunk && c0 + i < d.K; i += 32u) {
-      const double x = ch[i];
-      top4_insert(t, x, c0 + i);
-      tot += x;
-    }
+    for (uint32_t i = lane; i < kWbChunk && c0 + i < d.K; i += 32u) top4_insert(t, ch[i], c0 + i);
     __syncwarp();
   }
   WordRec r;
@@ -382,30 +329,18 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
     r.a[i] = ok ? bv : 0.0;
     r.K[i] = ok ? (uint16_t)bk : (uint16_t)0;
   }
-  tot = warp_sum(tot);
   const uint32_t K1 = r.K[0];
-  // scales: m = rint(What' 2^sh) with max What' = a2 in [2^31, 2^32) 2^-sh; qfx = rint(QP 2^t)
-  // with 2^t from the estimate of Q' (1 + 2^-30 covers its rounding: no entry saturates)
-  int e = 0;
-  frexp(r.a[1], &e);
-  const int sh = 32 - e;
-  int et = 0;
-  frexp(d.alpha * (tot - r.a[0]) * (1.0 + 0x1p-30), &et);
-  const double two_t = ldexp(1.0, 32 - et);
-  const bool out = v < d.Vw;
-  WrowPtrs o = wrow_ptrs(d, v);
-  // ---- pass 2: What' chunks -> m; lane 0's sequential Q' prefix -> QP, qfx, ce
+  // ---- pass 2: lane 0's sequential Q' = alpha sum_{k != K1} What[v][k] (ascending k: the
+  //      oracle's order, so Q' is its value bit for bit)
   double acc = 0.0;
+  double* qe = d.qexact + (size_t)v * d.nch;
   tcur = 0;
-  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += kWbChunk) {
+  for (uint32_t c0 = 0; c0 < d.K; c0 += kWbChunk) {
     fill_what_chunk(d, cur, v, c0, ch, tcur);
     if (lane == 0 && K1 >= c0 && K1 < c0 + kWbChunk) ch[K1 - c0] = 0.0;  // What' (Eq 6)
     __syncwarp();
-    const uint32_t n = min(kWbChunk, d.Kpad - c0);
-    if (out)
-      for (uint32_t i = lane; i < n; i += 32u) o.m[c0 + i] = __double2uint_rn(fmin(ldexp(ch[i], sh), 4294967295.0));
-    __syncwarp();
-    if (lane == 0) {  // strictly sequential (ascending k); 8 entries loaded ahead of the adds
+    const uint32_t n = min(kWbChunk, d.K - c0);
+    if (lane == 0) {  // strictly sequential; 8 entries loaded ahead of the dependent adds
       double x[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = ch[i];
@@ -415,39 +350,16 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
 #pragma unroll
         for (int i = 0; i < 8; ++i) xn[i] = ch[in + i];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc = acc + x[i];
-          ch[i0 + i] = d.alpha * acc;
-          if (c0 + i0 + i == d.K - 1u) r.Qp = d.alpha * acc;
-        }
+        for (int i = 0; i < 8; ++i)
+          if (i0 + i < n) acc = acc + x[i];
+        if ((i0 & 31u) == 24u || i0 + 8u >= n) qe[(c0 + i0) >> 5] = acc;  // exact P_v(32 c + 31)
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = xn[i];
       }
     }
     __syncwarp();
-    if (out) {
-      for (uint32_t i = lane; i < n; i += 32u) {
-        const double q = ch[i];
-        o.qp[c0 + i] = q;
-        o.qfx[c0 + i] = __double2uint_rn(fmin(q * two_t, 4294967295.0));
-      }
-      for (uint32_t i = 31u + 32u * lane; i < n; i += 32u * 32u) {  // chunk ends of this chunk
-        const uint32_t c = (c0 + i) >> 5;
-        o.ce[c] = (c < d.nch) ? __double2uint_rn(fmin(ch[i] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
-      }
-    }
-    __syncwarp();
   }
-  r.Qp = __shfl_sync(kFull, r.Qp, 0);
-  if (out) {
-    for (uint32_t c = d.nch + lane; c < ce_words(d.Kpad); c += 32u) o.ce[c] = 0xFFFFFFFFu;
-    if (lane == 0) {
-      o.sc[0] = ldexp(1.0, -sh);
-      o.sc[1] = ldexp(1.0, sh);
-      o.sc[2] = 1.0 / two_t;
-      o.sc[3] = two_t;
-    }
-  }
+  r.Qp = d.alpha * acc;
   if (lane == 0) d.rec[v] = r;
 }
 
@@ -864,15 +776,17 @@ __device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc,
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(bytes) : "memory");
+  const uint64_t g = (uint64_t)__cvta_generic_to_global(src);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
-               "l"(src), "r"(bytes), "r"(mbar_s)
+               "l"(g), "r"(bytes), "r"(mbar_s)
                : "memory");
 }
 
 // bulk copy completing on an mbarrier whose expect_tx was already posted
 __device__ __forceinline__ void bulk_copy_tx(uint32_t dst_s, const void* src, uint32_t bytes, uint32_t mbar_s) {
+  const uint64_t g = (uint64_t)__cvta_generic_to_global(src);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_s),
-               "l"(src), "r"(bytes), "r"(mbar_s)
+               "l"(g), "r"(bytes), "r"(mbar_s)
                : "memory");
 }
 
@@ -927,7 +841,7 @@ __device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint3
 // S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fast
 // path could not certify its decision.
 __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, const uint32_t* E,
-                               uint32_t nnz, double M, double u, const double* QP, bool& hitM) {
+                               uint32_t nnz, double M, double u, bool& hitM) {
   const uint32_t K1 = rec.K[0];
   double Sp = 0.0;
 #pragma unroll 4
@@ -957,15 +871,47 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
     }
     return last;
   }
+  // Q': the first k != K1 (ascending) with alpha P_v(k) > y, P_v the oracle's running sum of
+  // What over j <= k, j != K1; past the end -> last k != K1.  The word-prep kept the exact
+  // running sum at every 32nd topic (qe[c] = P_v(32 c + 31)): the first chunk whose end
+  // passes y is found by binary search, then the oracle's additions are replayed from the
+  // previous checkpoint through that chunk (same operands, same order: bit-identical)
   const double y = (x - M) - Sp;
-  uint32_t a = 0, b = d.Kpad - 1u;
-  while (a < b) {
-    const uint32_t mid = (a + b) >> 1;
-    if (QP[mid] > y) b = mid; else a = mid + 1u;
+  const double* qe = d.qexact + (size_t)v * d.nch;
+  uint32_t ca = 0, cb = d.nch;
+  while (ca < cb) {
+    const uint32_t mid = (ca + cb) >> 1;
+    if (d.alpha * qe[mid] > y) cb = mid; else ca = mid + 1u;
   }
-  if (a == K1 && QP[a] > y) ++a;  // only when K1 = 0 and y < 0
-  if (a >= d.K || !(QP[a] > y)) a = (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
-  return a;
+  if (ca >= d.nch) return (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
+  const bool dense = v < d.Vd;
+  const int32_t* wr = cur.Wd + (size_t)v * d.K;
+  const uint32_t* tr = dense ? nullptr : cur.Wt + d.tofs[v - d.Vd];
+  const uint32_t tn = dense ? 0u : cur.tnnz[v - d.Vd];
+  const uint32_t k0 = 32u * ca;
+  uint32_t te = 0;
+  if (!dense) {  // first tail entry with topic >= k0
+    uint32_t lo = 0, hi = tn;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if ((tr[mid] >> 16) < k0) lo = mid + 1u; else hi = mid;
+    }
+    te = lo;
+  }
+  double acc = ca ? qe[ca - 1u] : 0.0;
+  for (uint32_t k = k0; k < d.K; ++k) {
+    uint32_t c;
+    if (dense) {
+      c = (uint32_t)wr[k];
+    } else {
+      while (te < tn && (tr[te] >> 16) < k) ++te;
+      c = (te < tn && (tr[te] >> 16) == k) ? (tr[te] & 0xFFFFu) : 0u;
+    }
+    if (k == K1) continue;
+    acc = acc + ((double)c + d.beta) / d.den[k];
+    if (d.alpha * acc > y) return k;
+  }
+  return (d.K - 1 != K1) ? d.K - 1 : d.K - 2;
 }
 
 // One batch of flagged runs (warp-uniform control flow).  Returns the number of queue
@@ -981,7 +927,7 @@ template <uint32_t kSegW, uint32_t kSub, uint32_t kDTs, bool kQG>
 __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, const Buf& nxt, const WordRec& rec,
                                                  uint32_t v, uint32_t row_s, const uint32_t* qfx, const uint32_t* ce,
                                                  const double* scl,
-                                                 const double* const* qpp, uint32_t* hist, WarpScratch& ws,
+                                                 uint32_t* hist, WarpScratch& ws,
                                                  uint32_t qn, uint32_t iter, RunCounters& rc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
@@ -1259,7 +1205,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           uint32_t a = 0, b = d.Kpad - 1u;
           // the table is in the slot (shared memory) or, for large K (kQG), in HBM
           // (chunk ends ce in the slot either way: the HBM search touches one 128-byte line)
-          auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldg(qfx + i) : qfx[i]; };
+          // (HBM table: L1-cached loads, coherent within the SM -- a warp-staged item's table is
+          // written inside this kernel by a warp of the same block, published by the slot's
+          // release / acquire)
+          auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldca(qfx + i) : qfx[i]; };
           {  // first the 32-topic chunk from the contiguous chunk ends
             uint32_t ca = 0, cb = d.nch - 1u;
             while (ca < cb) {
@@ -1273,14 +1222,16 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             const uint32_t mid = (a + b) >> 1;
             if (qv(mid) > Yq) b = mid; else a = mid + 1u;
           }
-          const double mq = mg + inv_t;
+          // + one qfx ulp + the bound (K + 4) 2^-52 Q' on the difference between the staged
+          // chunked prefix and the oracle's sequential one (stage_row_warp)
+          const double mq = mg + inv_t + (double)(d.K + 4u) * 0x1p-52 * Qp;
           const double qa = (double)qv(a) * inv_t, qp = a ? (double)qv(a - 1u) * inv_t : 0.0;
           if (a != K1 && a < d.K && qa - y > mq && y - qp > mq) topic = a;
         }
       }
     }
     if (topic == 0xFFFFFFFFu) {
-      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, *qpp, hit);
+      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, hit);
       rc.exact += 1;
     }
     if (hit) rc.hitM += 1;
@@ -1320,8 +1271,7 @@ struct __align__(16) SlotCtl {
   uint32_t cursor, done;
   uint32_t sampled, hitM, runs, words, exact;
   uint32_t state;  // block item number held by the slot (| kExit: no item left)
-  const double* qp;    // exact Q' prefix table of the item's word (HBM)
-  const uint32_t* qfx; // fixed-point Q' prefix table (slot shared memory, or HBM if d.qfx_global)
+  const uint32_t* qfx; // fixed-point Q' prefix table (slot shared memory, or HBM scratch if d.qfx_global)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t* p) {
@@ -1343,71 +1293,104 @@ __host__ __device__ __forceinline__ uint32_t slot_head_bytes(uint32_t Kpad, uint
   return qfx_global ? 4u * Kpad + 32u + 4u * ce_words(Kpad) : 8u * Kpad + 32u + 4u * ce_words(Kpad);
 }
 
-// Tail-word row staged by one warp when word-prep did not precompute it (v >= Vw): the
-// fixed-point What' row, the sequential Q' prefix (the same expressions and order as
-// k_word_prep) into the slot's HBM scratch QP, its fixed-point copy and the scales.
-__device__ void stage_tail_row_warp(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, uint32_t* m,
-                                    uint32_t* qfx, uint32_t* ce, double* sc, double* QP) {
+// The item word's sampler head staged by one warp straight from W (no precomputed table):
+//   m[k]   = rint(What'[v][k] 2^s), What' = (W[v][k] + beta) * (1 / den_k) with the K1 entry 0
+//            (Eq 6); one rounding more than the oracle's quotient, so |m 2^-s - What'| < 2^-s
+//            still holds (the S' certification margin);
+//   qfx[k] = rint(alpha P'(k) 2^t), P' the fp64 prefix of What' in chunks of 32 topics (warp
+//            scan + running carry) -- another summation order than the oracle's sequential
+//            P_v, within (K + 4) 2^-52 Q' of it (standard fp64 summation bound, included in the
+//            Q' certification margin); ce[c] = qfx[32 c + 31] (chunk ends, in the slot);
+//   sc     = {2^-s, 2^s, 2^-t, 2^t} from a2 = max What' and Q' of the word record.
+// Tail words: the packed row's counts are first scattered into m (used as a count array).
+__device__ void stage_row_warp(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, uint32_t* m,
+                               uint32_t* qfx, uint32_t* ce, double* sc) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t K1 = rec.K[0];
-  for (uint32_t k0 = lane; k0 < d.Kpad; k0 += 256u) {  // 8 loads in flight per lane
-    double x[8];
-#pragma unroll
-    for (uint32_t i = 0; i < 8; ++i) {
-      const uint32_t k = k0 + 32u * i;
-      x[i] = (k < d.K) ? __ldg(d.what0 + k) : 0.0;
-    }
-#pragma unroll
-    for (uint32_t i = 0; i < 8; ++i)
-      if (k0 + 32u * i < d.Kpad) QP[k0 + 32u * i] = x[i];
-  }
-  __syncwarp();
-  const uint32_t t = v - d.Vd;
-  const uint32_t* tr = cur.Wt + d.tofs[t];
-  const uint32_t n = cur.tnnz[t];
-  for (uint32_t e = lane; e < n; e += 32u) {
-    const uint32_t p = tr[e];
-    const uint32_t k = p >> 16;
-    QP[k] = ((double)(p & 0xFFFFu) + d.beta) / d.den[k];
-  }
-  __syncwarp();
-  if (lane == 0) QP[K1] = 0.0;  // What' (Eq 6)
-  __syncwarp();
   int e = 0;
   frexp(rec.a[1], &e);
-  const int sh = 32 - e;
-  for (uint32_t k = lane; k < d.Kpad; k += 32u) m[k] = __double2uint_rn(fmin(ldexp(QP[k], sh), 4294967295.0));
-  __syncwarp();
-  if (lane == 0) {
-    double acc = 0.0;
-#pragma unroll 16
-    for (uint32_t k = 0; k < d.Kpad; ++k) {
-      acc = acc + QP[k];
-      QP[k] = acc;
-    }
-  }
-  __syncwarp();
-  for (uint32_t k = lane; k < d.Kpad; k += 32u) QP[k] = d.alpha * QP[k];
+  const int sh = 32 - e;  // max What' 2^sh in [2^31, 2^32)
+  const double two_s = ldexp(1.0, sh);
   int et = 0;
   frexp(rec.Qp, &et);
-  const double two_t = ldexp(1.0, 32 - et);
-  __syncwarp();
-  for (uint32_t k = lane; k < d.Kpad; k += 32u) qfx[k] = __double2uint_rn(fmin(QP[k] * two_t, 4294967295.0));
-  for (uint32_t c = lane; c < ce_words(d.Kpad); c += 32u)  // chunk ends (in the slot)
-    ce[c] = (c < d.nch) ? __double2uint_rn(fmin(QP[32u * c + 31u] * two_t, 4294967295.0)) : 0xFFFFFFFFu;
+  const double two_t = ldexp(1.0, 32 - et);  // Q' 2^t in [2^31, 2^32)
+  const bool dense = v < d.Vd;
+  const int32_t* wr = cur.Wd + (size_t)v * d.K;
+  if (!dense) {
+    for (uint32_t k = lane; k < d.Kpad; k += 32u) m[k] = 0u;
+    __syncwarp();
+    const uint32_t t = v - d.Vd;
+    const uint32_t* tr = cur.Wt + d.tofs[t];
+    const uint32_t n = cur.tnnz[t];
+    for (uint32_t i = lane; i < n; i += 32u) {
+      const uint32_t p = tr[i];
+      m[p >> 16] = p & 0xFFFFu;
+    }
+    __syncwarp();
+  }
+  double carry = 0.0;
+  constexpr uint32_t kU = 4;  // chunks in flight per step
+  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += 32u * kU) {
+    uint32_t cnt[kU];
+    double id[kU];
+#pragma unroll
+    for (uint32_t u = 0; u < kU; ++u) {
+      const uint32_t k = c0 + 32u * u + lane;
+      const bool in = k < d.K;
+      cnt[u] = in ? (dense ? (uint32_t)__ldg(wr + k) : m[k]) : 0u;
+      id[u] = in ? __ldg(d.inv_den + k) : 0.0;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kU; ++u) {
+      const uint32_t k = c0 + 32u * u + lane;
+      if (k >= d.Kpad) break;  // warp-uniform (Kpad is a multiple of 32)
+      const double w = (k < d.K && k != K1) ? ((double)cnt[u] + d.beta) * id[u] : 0.0;
+      m[k] = __double2uint_rn(fmin(w * two_s, 4294967295.0));
+      double x = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(kFull, x, o);
+        if (lane >= (uint32_t)o) x = x + y;
+      }
+      const uint32_t q = __double2uint_rn(fmin(d.alpha * (carry + x) * two_t, 4294967295.0));
+      qfx[k] = q;
+      if (lane == 31u) ce[k >> 5] = q;
+      carry = carry + __shfl_sync(kFull, x, 31);
+    }
+  }
+  for (uint32_t c = d.nch + lane; c < ce_words(d.Kpad); c += 32u) ce[c] = 0xFFFFFFFFu;
   if (lane == 0) {
-    sc[0] = ldexp(1.0, -sh);
-    sc[1] = ldexp(1.0, sh);
-    sc[2] = ldexp(1.0, et - 32);
+    sc[0] = 1.0 / two_s;
+    sc[1] = two_s;
+    sc[2] = 1.0 / two_t;
     sc[3] = two_t;
   }
   __syncwarp();
 }
 
+// Sampler head of word v in the wrow table (v < Vw; k_word_heads): m | scales | qfx | ce.
+struct HeadPtrs {
+  uint32_t* m;
+  double* sc;
+  uint32_t* qfx;
+  uint32_t* ce;
+};
+__device__ __forceinline__ HeadPtrs head_ptrs(const Dev& d, uint32_t v) {
+  unsigned char* b = d.wrow + (size_t)v * d.rs_bytes;
+  HeadPtrs o;
+  o.m = reinterpret_cast<uint32_t*>(b);
+  o.sc = reinterpret_cast<double*>(b + 4u * d.Kpad);
+  o.qfx = reinterpret_cast<uint32_t*>(b + 4u * d.Kpad + 32u);
+  o.ce = o.qfx + d.Kpad;
+  return o;
+}
+
 // Arm slot `sl` with block item k (one warp): claim the next global item, publish its
-// description, start the What' row transfer.  The slot's histogram is zero on entry.
-__device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char* sbase, double* qp_scratch, uint32_t k,
-                         uint32_t n_items) {
+// description and fill the slot with the word's head: ONE TMA bulk copy (cp.async.bulk,
+// completing on the slot's mbarrier) of the precomputed head (v < Vw), else staged by this
+// warp (stage_row_warp) followed by a plain arrive.  The slot's histogram is zero on entry.
+__device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char* sbase, uint32_t* qfx_scratch,
+                         uint32_t k, uint32_t n_items) {
   const uint32_t lane = threadIdx.x & 31u;
   uint32_t i = 0;
   if (lane == 0) i = (uint32_t)atomicAdd(&d.ctr->item_ctr, 1ull);
@@ -1434,34 +1417,48 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
     c.words = 0;
     c.exact = 0;
   }
-  if (v < d.Vw) {  // precomputed by word-prep
+  if (v < d.Vw) {  // precomputed by k_word_heads
     if (lane == 0) {
-      const WrowPtrs o = wrow_ptrs(d, v);
-      c.qp = o.qp;
-      c.qfx = d.qfx_global ? o.qfx : mrow + d.Kpad + 8u;
+      const HeadPtrs o = head_ptrs(d, v);
+      const uint32_t ms = (uint32_t)__cvta_generic_to_shared(mrow);
       if (!d.qfx_global) {  // m | scales | qfx | ce: one contiguous bulk copy
-        bulk_g2s((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs,
-                 slot_head_bytes(d.Kpad, 0u), mbar_s);
+        c.qfx = mrow + d.Kpad + 8u;
+        bulk_g2s(ms, o.m, slot_head_bytes(d.Kpad, 0u), mbar_s);
       } else {  // m | scales, then the chunk ends ce (the qfx table itself stays in HBM)
+        c.qfx = o.qfx;
         const uint32_t b1 = 4u * d.Kpad + 32u, b2 = 4u * ce_words(d.Kpad);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s), "r"(b1 + b2) : "memory");
-        bulk_copy_tx((uint32_t)__cvta_generic_to_shared(mrow), d.wrow + (size_t)v * d.rs, b1, mbar_s);
-        bulk_copy_tx((uint32_t)__cvta_generic_to_shared(mrow) + b1, o.ce, b2, mbar_s);
+        bulk_copy_tx(ms, o.m, b1, mbar_s);
+        bulk_copy_tx(ms + b1, o.ce, b2, mbar_s);
       }
     }
   } else {
-    uint32_t* qfx = d.qfx_global ? reinterpret_cast<uint32_t*>(qp_scratch + d.Kpad) : mrow + d.Kpad + 8u;
-    if (lane == 0) {
-      c.qp = qp_scratch;
-      c.qfx = qfx;
-    }
     __syncwarp();
+    // slot: m | scales | qfx | ce, or m | scales | ce with qfx in the slot's HBM scratch
+    uint32_t* qfx = d.qfx_global ? qfx_scratch : mrow + d.Kpad + 8u;
     uint32_t* ce = d.qfx_global ? mrow + d.Kpad + 8u : qfx + d.Kpad;
-    stage_tail_row_warp(d, cur, v, c.rec, mrow, qfx, ce, reinterpret_cast<double*>(mrow + d.Kpad), qp_scratch);
+    if (lane == 0) c.qfx = qfx;
+    stage_row_warp(d, cur, v, c.rec, mrow, qfx, ce, reinterpret_cast<double*>(mrow + d.Kpad));
+    if (d.qfx_global) __threadfence_block();  // the HBM qfx table before the arrive / release
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar_s) : "memory");
   }
   __syncwarp();
   if (lane == 0) st_release_s(&c.state, k);
+}
+
+// H1 (second half): the sampler heads of this iteration's words (the words of the live items
+// when the per-iteration schedule runs, else every word; v < Vw) into the wrow table, one
+// warp per word -- the same staging as an in-kernel item (stage_row_warp), written to HBM
+// for the sampler's bulk copies.
+__global__ void __launch_bounds__(128) k_word_heads(Dev d, Buf cur) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t v = blockIdx.x * 4u + (threadIdx.x >> 5);
+  if (v >= d.Vw || d.wtok[v + 1] == d.wtok[v]) return;
+  if (d.word_live && !d.word_live[v]) return;
+  (void)lane;
+  const WordRec r = d.rec[v];
+  const HeadPtrs o = head_ptrs(d, v);
+  stage_row_warp(d, cur, v, r, o.m, o.qfx, o.ce, o.sc);
 }
 
 // Warp-level epilogue of a finished item: skipped tokens at K1, W row / n_k from the
@@ -1495,7 +1492,6 @@ __device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uin
       if (n) {
         if (dense) atomicAdd(&Wrow[k], (int32_t)n);
         else out[nz + __popc(m & lanemask_lt())] = (k << 16) | n;
-        atomicAdd(&nxt.nk[k], (int32_t)n);
         hist[k] = 0;
       }
       nz += __popc(m);
@@ -1517,7 +1513,6 @@ __device__ void item_epilogue_warp(const Dev& d, const Buf& nxt, SlotCtl& c, uin
       const uint32_t n = hist[k];
       if (dense) atomicAdd(&Wrow[k], (int32_t)n);
       else out[pos++] = (k << 16) | n;
-      atomicAdd(&nxt.nk[k], (int32_t)n);
       hist[k] = 0;
     }
     if (b) bmp[wi] = 0;
@@ -1570,9 +1565,9 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     return d.hist_global ? d.hist_scratch + ((size_t)blockIdx.x * nsl + sl) * (d.Kpad + d.Kpad / 32u)
                          : reinterpret_cast<uint32_t*>(slots + sl * sb + slot_head_bytes(d.Kpad, d.qfx_global));
   };
-  // exact QP [Kpad] f64 (+ qfx [Kpad] u32 when d.qfx_global) of a warp-staged tail row
-  auto qps_of = [&](uint32_t sl) -> double* {
-    return d.qp_scratch + ((size_t)blockIdx.x * nsl + sl) * qp_scratch_stride(d.Kpad);
+  // fixed-point Q' table of slot sl in HBM (d.qfx_global: large K)
+  auto qfs_of = [&](uint32_t sl) -> uint32_t* {
+    return d.qfx_global ? d.qfx_scratch + ((size_t)blockIdx.x * nsl + sl) * d.Kpad : nullptr;
   };
   const uint32_t nw = blockDim.x >> 5;
   // prologue: barriers, zero histograms, warp 0 arms the first kSlots items
@@ -1591,7 +1586,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     }
   __syncthreads();
   if (warp == 0)
-    for (uint32_t sl = 0; sl < nsl; ++sl) arm_slot(d, cur, ctl[sl], slots + sl * sb, qps_of(sl), sl, n_items);
+    for (uint32_t sl = 0; sl < nsl; ++sl) arm_slot(d, cur, ctl[sl], slots + sl * sb, qfs_of(sl), sl, n_items);
   for (uint32_t k = 0;; ++k) {
     const uint32_t sl = k % nsl;
     SlotCtl& c = ctl[sl];
@@ -1652,11 +1647,11 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
         pf_fw = (lane < G && pf_rb + lane < r1) ? d.flags[(pf_rb + lane) >> 5] : 0u;
         pf_ok = true;
       }
-      uint32_t nb = sample_batch<kSegW, kSub, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, &c.qp, hist, ws,
+      uint32_t nb = sample_batch<kSegW, kSub, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl, hist, ws,
                                                          qn, iter, rc);
       if (kFbW && nb == 0)  // a run with more than kSegCap x 16 nonzeros (large K only): wide segments
         nb = sample_batch<kFbW ? kFbW : 16u, kFbW ? kFbW : 16u, kDTs, kQG>(d, cur, nxt, rec, v, row_s, qfx, ce, scl,
-                                                                          &c.qp, hist, ws, qn, iter, rc);
+                                                                          hist, ws, qn, iter, rc);
 
       // drop the processed runs from the queue (ring)
       ws.head += nb;
@@ -1679,7 +1674,7 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     last = __shfl_sync(kFull, last, 0);
     if (last) {
       item_epilogue_warp(d, nxt, c, hist);
-      arm_slot(d, cur, c, slots + sl * sb, qps_of(sl), k + nsl, n_items);
+      arm_slot(d, cur, c, slots + sl * sb, qfs_of(sl), k + nsl, n_items);
     }
   }
 }
@@ -1693,19 +1688,12 @@ __device__ void item_epilogue(const Dev& d, const Buf& nxt, uint32_t v, const ui
     int32_t* Wrow = nxt.Wd + (size_t)v * d.K;
     for (uint32_t k = tid; k < d.K; k += blockDim.x) {
       const uint32_t c = hist[k];
-      if (c) {
-        atomicAdd(&Wrow[k], (int32_t)c);
-        atomicAdd(&nxt.nk[k], (int32_t)c);
-      }
+      if (c) atomicAdd(&Wrow[k], (int32_t)c);
     }
   } else {
     const uint32_t t = v - d.Vd;
     const uint32_t nz = block_compact(hist, d.K, nxt.Wt + d.tofs[t], s_wsum, s_run, 16u);
     if (tid == 0) nxt.tnnz[t] = nz;
-    for (uint32_t k = tid; k < d.K; k += blockDim.x) {
-      const uint32_t c = hist[k];
-      if (c) atomicAdd(&nxt.nk[k], (int32_t)c);
-    }
   }
 }
 
@@ -1725,6 +1713,48 @@ __global__ void __launch_bounds__(256) k_wcount(Dev d, Buf cur, Buf nxt) {
   }
   __syncthreads();
   item_epilogue(d, nxt, v, hist, s_wsum, &s_run);
+}
+
+// H6: n_k = sum_v W[v][k] once W is complete (after the sampler, and after the H7 merge
+// when world > 1): column sums of the dense block (consecutive threads read consecutive
+// topics of a row: coalesced) and the tail rows' packed entries, reduced per block in shared
+// memory, then one atomic per (block, topic) -- no per-(item, topic) global atomics.
+constexpr uint32_t kNkBlocks = 296;
+__global__ void __launch_bounds__(256) k_nk(Dev d, Buf b) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_nk = reinterpret_cast<uint32_t*>(smem);
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  for (uint32_t k = tid; k < d.Kpad; k += blockDim.x) s_nk[k] = 0u;
+  __syncthreads();
+  const uint32_t rpb = (d.Vd + gridDim.x - 1u) / gridDim.x;  // dense rows of this block
+  const uint32_t v0 = min(d.Vd, blockIdx.x * rpb), v1 = min(d.Vd, v0 + rpb);
+  for (uint32_t k = tid; k < d.K; k += blockDim.x) {  // thread-owned topics: plain adds
+    uint32_t acc = 0;
+    const int32_t* col = b.Wd + k;
+    uint32_t v = v0;
+    for (; v + 4u <= v1; v += 4u)
+      acc += (uint32_t)col[(size_t)v * d.K] + (uint32_t)col[(size_t)(v + 1u) * d.K] +
+             (uint32_t)col[(size_t)(v + 2u) * d.K] + (uint32_t)col[(size_t)(v + 3u) * d.K];
+    for (; v < v1; ++v) acc += (uint32_t)col[(size_t)v * d.K];
+    s_nk[k] = acc;
+  }
+  __syncthreads();
+  const uint32_t Vt = d.V - d.Vd;
+  const uint32_t tpb = (Vt + gridDim.x - 1u) / gridDim.x;  // tail words of this block
+  const uint32_t t0 = min(Vt, blockIdx.x * tpb), t1 = min(Vt, t0 + tpb);
+  for (uint32_t t = t0 + warp; t < t1; t += blockDim.x >> 5) {
+    const uint32_t* tr = b.Wt + d.tofs[t];
+    const uint32_t n = b.tnnz[t];
+    for (uint32_t e = lane; e < n; e += 32u) {
+      const uint32_t p = tr[e];
+      atomicAdd(&s_nk[p >> 16], p & 0xFFFFu);
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = tid; k < d.K; k += blockDim.x) {
+    const uint32_t n = s_nk[k];
+    if (n) atomicAdd(&b.nk[k], (int32_t)n);
+  }
 }
 
 // H7 (world > 1): global packed tail row of tail word t from every rank's word-major tail
@@ -1773,6 +1803,7 @@ __global__ void __launch_bounds__(256) k_item_schedule(Dev d, Buf nxt, uint32_t 
   const uint32_t any = __any_sync(kFull, f != 0u) ? 1u : 0u;
   if (lane == 0) {
     d.item_live[item] = (uint8_t)any;
+    if (any && d.word_live) d.word_live[d.item_word[item]] = 1u;  // its head is needed (k_word_heads)
     if (!any) {
       const uint32_t v = d.item_word[item], n = d.item_ntok[item], K1 = d.rec[v].K[0];
       if (v < d.Vd) {
@@ -1781,7 +1812,6 @@ __global__ void __launch_bounds__(256) k_item_schedule(Dev d, Buf nxt, uint32_t 
         nxt.Wt[d.tofs[v - d.Vd]] = (K1 << 16) | n;
         nxt.tnnz[v - d.Vd] = 1u;
       }
-      atomicAdd(&nxt.nk[K1], (int32_t)n);
     }
   }
 }
@@ -2017,10 +2047,6 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
   const uint32_t nch = (K + 31) / 32;
   return (size_t)nch * 32 * 8 + (size_t)nch * 8 + (size_t)(nch + 1) * 8;
 }
-uint32_t wrow_stride(uint32_t K) {  // m | scales | qfx | ce | QP (doubles)
-  const uint32_t Kpad = (K + 31) / 32 * 32;
-  return 2u * Kpad + 4u + ce_words(Kpad) / 2u;
-}
 #ifndef EZLDA_SEG_MIN
 #define EZLDA_SEG_MIN 16
 #endif
@@ -2111,7 +2137,6 @@ static const void* sampler_kernel(uint32_t K, uint32_t qg) {
     default: return sampler_kernel_fb<256u, kDTLarge>(qg);
   }
 }
-uint32_t sampler_qp_scratch_stride(uint32_t Kpad) { return qp_scratch_stride(Kpad); }
 
 size_t word_prep_smem_bytes(uint32_t K) { return (size_t)kWpWarps * ((K + 31) / 32) * 32 * 8; }  // row per warp
 
@@ -2154,6 +2179,7 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   if (nb < 1) return cudaErrorInvalidConfiguration;
   *grid = (uint32_t)(nsm * nb);
   if ((e = raise_smem(dev, (const void*)k_wcount, (int)wcount_smem_bytes(K)))) return e;
+  if ((e = raise_smem(dev, (const void*)k_nk, (int)wcount_smem_bytes(K)))) return e;
   if ((e = raise_smem(dev, (const void*)k_tail_rebuild, (int)wcount_smem_bytes(K)))) return e;
   if (two_branch_word_major(K) && (e = raise_smem(dev, (const void*)k_tb_item, (int)tb_item_smem_bytes(K))))
     return e;
@@ -2169,6 +2195,14 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
 
 void launch_den(const Dev& d, const Buf& cur, cudaStream_t s) {
   k_den<<<(d.K + 255) / 256, 256, 0, s>>>(d, cur);
+}
+
+void launch_word_heads(const Dev& d, const Buf& cur, cudaStream_t s) {
+  if (d.Vw) k_word_heads<<<(d.Vw + 3u) / 4u, 128, 0, s>>>(d, cur);
+}
+uint32_t head_bytes(uint32_t K) {  // m | scales | qfx | ce of one word (a multiple of 16 bytes)
+  const uint32_t Kpad = (K + 31u) / 32u * 32u;
+  return 8u * Kpad + 32u + 4u * ce_words(Kpad);
 }
 
 void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s) {
@@ -2230,6 +2264,10 @@ void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_
   k_tb_prep<<<d.V, 256, 0, s>>>(d, cur);
   k_tb_draw<<<(d.Dn + 7) / 8, 256, 0, s>>>(d, nxt, iteration);
   if (n_items) k_wcount<<<n_items, 256, wcount_smem_bytes(d.K), s>>>(d, nxt, nxt);
+}
+
+void launch_nk(const Dev& d, const Buf& b, cudaStream_t s) {
+  k_nk<<<kNkBlocks, 256, 4u * d.Kpad, s>>>(d, b);
 }
 
 void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, const uint32_t* off, uint32_t world,

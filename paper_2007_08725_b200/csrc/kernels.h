@@ -18,10 +18,10 @@
 //   W: dense rows int32 [Vd x K] for words v < Vd, packed sparse tail rows (capacity
 //     min(c_v, K) at tofs[v-Vd]) with tnnz[v-Vd]; double-buffered with n_k[K].
 //   rec[V] WordRec (48 B): top-4 topics/values and Q' of every word.
-//   wrow[Vw][rs]: per word u32 m[Kpad] (fixed-point What', K1 entry 0) | f64 {2^-s, 2^s,
-//     2^-t, 2^t} | u32 qfx[Kpad] (fixed-point Q' prefix) | f64 QP[Kpad] (exact Q' prefix)
-//     -- written by word-prep; the head (m | scales [| qfx]) is bulk-copied (TMA) into a
-//     sampler slot, QP is read by the exact redraws.
+//   wrow[Vw][rs_bytes]: sampler heads of the words with a live item: u32 m[Kpad] (fixed-point
+//     What', K1 entry 0) | f64 {2^-s, 2^s, 2^-t, 2^t} | u32 qfx[Kpad] (fixed-point Q' prefix)
+//     | u32 ce[] (its chunk ends); bulk-copied (TMA) into a sampler slot.  Words v >= Vw (when
+//     V heads do not fit in HBM) are staged by a sampler warp (stage_row_warp).
 //   items: (word, run range, tokens): the sampler's work list, heavy first.
 #pragma once
 #include <cstdint>
@@ -61,17 +61,15 @@ struct Dev {
   uint32_t qfx_global;   // 1 (large K): the fixed-point Q' table is searched in HBM, not staged  // 1 (K >= 2048): item epilogues visit only the topics marked in a bitmap
   uint32_t slot_bytes, ws_bytes;  // sampler shared-memory layout
   uint32_t* hist_scratch;  // [grid * nslots * Kpad] (zero between items)
-  double* qp_scratch;      // [grid * nslots * 1.5 Kpad] exact Q' (+ fixed-point) tables of warp-staged tail rows
+  uint32_t* qfx_scratch;   // [grid * nslots * Kpad] fixed-point Q' tables in HBM (qfx_global)
   uint32_t exact_all;  // 1: every sampled token takes the exact fp64 path (test/ablation knob)
   uint32_t branches;   // 3: three-branch sampler (default); 2: two-branch ESCA mode (NEXT-1)
   double* tbw;         // two-branch mode: [V * Kpad] What rows (Eq 1-2)
   double* tbq;         // two-branch mode: [V * Kpad] Q tree prefix sum_{j<=k} alpha What_j
-  uint32_t Vw;     // words v < Vw have their What' | QP row precomputed in wrow (Vd, or V if it fits)
   uint32_t zmark;  // K <= 32768: the doc pass marks z^i of a failing token as 0x8000 | min(C1, c1_cap)
   uint32_t c1_cap; // 0x7FFF; a marker equal to it sends the sampler to the packed-row lookup of C1 (debug
                    // flag EZLDA_DEBUG_C1_LOOKUP sets it to 0: every failing token takes the lookup)
   uint32_t sampler_grid;  // persistent sampler grid of this handle (SMs x resident blocks, configure_kernels)
-  uint32_t rs;    // wrow stride in doubles (Kpad + nch + 1, rounded up to 2)
   uint32_t segw;  // entries per S' segment (power of two >= 16; ceil(K / segw) <= kSegCap)
   uint32_t segsub;  // entries per S' checkpoint chunk (8: one per sector; or segw)
   uint32_t segfb;   // fallback segment width for runs longer than kSegCap x segw (0: none)
@@ -102,9 +100,14 @@ struct Dev {
   uint32_t* D;
   uint32_t* flags;
   WordRec* rec;
-  double* wrow;   // [Vw * rs] precomputed What' rows + Q' prefix tables (words v < Vw)
   double* den;    // [K] n_k + V beta
   double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
+  double* inv_den;  // [K] 1 / den_k (the sampler's fixed-point heads, stage_row_warp)
+  double* qexact;   // [V * nch] exact running sums P_v(32 c + 31) of the word-prep (exact redraws)
+  unsigned char* wrow;  // [Vw * rs_bytes] sampler heads m | scales | qfx | ce (k_word_heads)
+  uint32_t Vw;          // words v < Vw have a precomputed head (V, or Vd when V heads do not fit)
+  uint32_t rs_bytes;    // head_bytes(K)
+  uint8_t* word_live;   // [V] 1 iff the word has a live item this iteration (nullptr: every word)
   Counters* ctr;
 };
 
@@ -119,7 +122,9 @@ struct Buf {
 
 // ----- per-iteration kernels -----
 void launch_den(const Dev& d, const Buf& cur, cudaStream_t s);
-void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s);
+void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s);  // word records (top-4, Q')
+void launch_word_heads(const Dev& d, const Buf& cur, cudaStream_t s);  // sampler heads of live words
+uint32_t head_bytes(uint32_t K);
 // doc pass over the two length tiers; skip_test=false only rebuilds D (for counts/loglik)
 void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_t* docs_w, uint32_t n_w,
                      const uint32_t* docs_b, uint32_t n_b, uint32_t iteration, bool skip_test, cudaStream_t s);
@@ -136,6 +141,9 @@ void launch_item_schedule(const Dev& d, const Buf& nxt, uint32_t n_items, cudaSt
 void launch_two_branch(const Dev& d, const Buf& cur, const Buf& nxt, uint32_t n_items, uint32_t iteration,
                        cudaStream_t s);
 bool two_branch_word_major(uint32_t K);
+// H6: n_k = sum_v W[v][k] of the completed W (column sums of the dense block + the tail rows'
+// entries): a two-level reduction, per block in shared memory then one atomic per (block, topic)
+void launch_nk(const Dev& d, const Buf& b, cudaStream_t s);
 // H7 (world > 1): global tail rows from every rank's all-gathered word-major tail topics
 void launch_tail_rebuild(const Dev& d, const Buf& nxt, const uint16_t* tz_all, const uint32_t* off, uint32_t world,
                          uint64_t tail_max, cudaStream_t s);
@@ -157,8 +165,6 @@ struct SamplerLayout {
   size_t smem_bytes;
 };
 SamplerLayout sampler_layout(uint32_t K);
-uint32_t sampler_qp_scratch_stride(uint32_t Kpad);  // doubles per slot of qp_scratch
-uint32_t wrow_stride(uint32_t K);
 void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb);
 uint32_t sampler_group_runs(uint32_t K);
 size_t doc_block_smem_bytes(uint32_t K);

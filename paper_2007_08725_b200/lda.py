@@ -47,6 +47,7 @@ class IterStats(C.Structure):
         ("active_runs", C.c_uint64), ("drow_words", C.c_uint64), ("d_nnz", C.c_uint64),
         ("model_bytes", C.c_double), ("model_bytes_sample", C.c_double), ("model_bytes_docpass", C.c_double),
         ("kernel_launches", C.c_uint64), ("exact_redraws", C.c_uint64), ("exchange_bytes", C.c_double),
+        ("ms_sampler_kernel", C.c_double),
     ]
 
     def as_dict(self) -> dict:
