@@ -19,6 +19,12 @@ struct __align__(16) WordRec {
   uint16_t K[4];
 };
 
+// The doc pass's view of a word record (g <= 2): a1..a3 and Q' in one 32-byte aligned record
+// (one 256-bit load per token instead of three 128-bit loads) and K1 | K2 << 16 beside it.
+struct __align__(32) WordRecM {
+  double a0, a1, a2, Qp;
+};
+
 // ---------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11).  Counter (t_g lo, t_g hi, iteration, 0),
 // key = seed (lo, hi).
@@ -40,6 +46,38 @@ __device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32
 __device__ __forceinline__ double philox_u(uint64_t seed, uint32_t iteration, uint64_t tg) {
   uint32_t c0 = (uint32_t)tg, c1 = (uint32_t)(tg >> 32), c2 = iteration, c3 = 0u;
   philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t bits = ((uint64_t)(c0 >> 5) << 26) | (uint64_t)(c1 >> 6);
+  return (double)bits * 0x1p-53;
+}
+
+// Round keys of Philox4x32-10 for one seed: key[2 r] = seed lo + r 0x9E3779B9, key[2 r + 1] =
+// seed hi + r 0xBB67AE85 (r = 0..9), precomputed on the host so that the ten rounds take them as
+// constant-bank operands instead of recomputing the key schedule per draw.
+struct PhiloxKeys {
+  uint32_t k[20];
+};
+inline PhiloxKeys philox_keys(uint64_t seed) {
+  PhiloxKeys p;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    p.k[2 * r] = k0;
+    p.k[2 * r + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return p;
+}
+
+// philox_u with precomputed round keys (identical output)
+__device__ __forceinline__ double philox_u_k(const PhiloxKeys& K, uint32_t iteration, uint64_t tg) {
+  uint32_t c0 = (uint32_t)tg, c1 = (uint32_t)(tg >> 32), c2 = iteration, c3 = 0u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ K.k[2 * r], n2 = hi0 ^ c3 ^ K.k[2 * r + 1];
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
   const uint64_t bits = ((uint64_t)(c0 >> 5) << 26) | (uint64_t)(c1 >> 6);
   return (double)bits * 0x1p-53;
 }

@@ -145,9 +145,10 @@ __global__ void k_run_tables(const uint32_t* rperm, uint32_t R, uint32_t N, cons
   }
 }
 
-__global__ void k_trid(const uint32_t* qinc, const uint32_t* rid_of_q, uint32_t n, uint32_t* trid) {
+// (word, run id) of every doc-major token, packed for one 8-byte load in the doc pass
+__global__ void k_twr(const uint32_t* qinc, const uint32_t* rid_of_q, const uint32_t* tw, uint32_t n, uint2* twr) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) trid[j] = rid_of_q[qinc[j] - 1];
+  if (j < n) twr[j] = make_uint2(tw[j], rid_of_q[qinc[j] - 1]);
 }
 
 // wrun[v] = first run of word v (lower bound in the sorted run words), v in [0, V]
@@ -542,6 +543,7 @@ void fill_dev(ezlda* h) {
   d.beta = h->beta;
   d.Vbeta = (double)h->V * h->beta;
   d.seed = h->seed;
+  d.pk = ezl::philox_keys(h->seed);
 }
 
 // W^cur and n_k^cur from buf[cur].z (init / set_topics), + all-reduce
@@ -725,7 +727,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(rkey_out);
   h->release(q_iota);
   h->release(q_v);
-  uint32_t *d_dofs, *d_ddb, *run_j0, *run_dbase, *len32, *rid_of_q, *trid;
+  uint32_t *d_dofs, *d_ddb, *run_j0, *run_dbase, *len32, *rid_of_q;
+  uint2* twr;
   uint16_t* run_len;
   EZ_ALLOC(h, d_dofs, uint32_t, h->Dn + 1);
   EZ_CUDA(h, cudaMemcpyAsync(d_dofs, dofs.data(), sizeof(uint32_t) * (h->Dn + 1), cudaMemcpyHostToDevice, s));
@@ -740,8 +743,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(q_j0);
   h->release(q_doc);
   h->release(rperm);
-  EZ_ALLOC(h, trid, uint32_t, N);
-  k_trid<<<blocks(N), 256, 0, s>>>(qinc, rid_of_q, N, trid);
+  EZ_ALLOC(h, twr, uint2, N);
+  k_twr<<<blocks(N), 256, 0, s>>>(qinc, rid_of_q, tw, N, twr);
   h->release(qinc);
   h->release(rid_of_q);
   // ---- items: per word, split dense words every split_threshold tokens
@@ -879,7 +882,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   d.dofs = d_dofs;
   d.ddb = d_ddb;
   d.tw = tw;
-  d.trid = trid;
+  d.twr = twr;
   d.run_j0 = run_j0;
   d.run_dbase = run_dbase;
   d.run_len = run_len;
@@ -905,6 +908,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.D, uint32_t, h->Dwords);
   EZ_ALLOC(h, d.flags, uint32_t, (R + 31) / 32);
   EZ_ALLOC(h, d.rec, ezl::WordRec, h->V);
+  EZ_ALLOC(h, d.recm, ezl::WordRecM, h->V);
+  EZ_ALLOC(h, d.reck, uint32_t, h->V);
   EZ_ALLOC(h, d.qexact, double, (size_t)h->V * d.nch);
   // sampler heads (8 Kpad + 32 + ce bytes per word) for every word when they fit in half of
   // the free device memory (at most 64 GiB), else for the dense words only (the other items
@@ -936,6 +941,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     EZ_ALLOC(h, B.nk, int32_t, h->K);
   }
   EZ_CUDA(h, cudaMemsetAsync(d.rec, 0, sizeof(ezl::WordRec) * h->V, s));
+  EZ_CUDA(h, cudaMemsetAsync(d.recm, 0, sizeof(ezl::WordRecM) * h->V, s));
+  EZ_CUDA(h, cudaMemsetAsync(d.reck, 0, sizeof(uint32_t) * h->V, s));
   EZ_ALLOC(h, h->llpt_partial, double, std::max<uint32_t>(NI, 1));
   EZ_ALLOC(h, h->llpt_out, double, 1);
   EZ_CUDA(h, cudaMallocHost(&h->ctr_host, sizeof(ezl::Counters) * ezlda::kSlots));

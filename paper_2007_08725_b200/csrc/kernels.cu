@@ -243,6 +243,8 @@ __global__ void __launch_bounds__(kWpWarps * 32) k_word_prep_w(Dev d, Buf cur) {
     }
     r.Qp = d.alpha * acc;
     d.rec[v] = r;
+    d.recm[v] = WordRecM{r.a[0], r.a[1], r.a[2], r.Qp};
+    d.reck[v] = (uint32_t)r.K[0] | ((uint32_t)r.K[1] << 16);
   }
 }
 
@@ -360,7 +362,11 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
     __syncwarp();
   }
   r.Qp = d.alpha * acc;
-  if (lane == 0) d.rec[v] = r;
+  if (lane == 0) {
+    d.rec[v] = r;
+    d.recm[v] = WordRecM{r.a[0], r.a[1], r.a[2], r.Qp};
+    d.reck[v] = (uint32_t)r.K[0] | ((uint32_t)r.K[1] << 16);
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -376,11 +382,26 @@ __device__ __forceinline__ uint32_t row_lookup(const uint16_t* keys, const uint1
   return (lo < n && keys[lo] == k) ? cnts[lo] : 0u;
 }
 
-// MPT test of one token j (word v, run rid) of a doc of length L.  C(k) = D[d][k].
+// MPT test of one token j (word v) of a doc of length L.  C(k) = D[d][k].  Writes z^i (K1, or
+// the sampler's marker) and returns true if the token failed the test (its run must be flagged).
 template <typename LookupF>
-__device__ __forceinline__ void mpt_token(const Dev& d, const Buf& nxt, uint32_t j, uint32_t L, uint32_t iter,
-                                          uint32_t v, uint32_t rid, LookupF C, unsigned long long& n_skip) {
-  const WordRec r = d.rec[v];
+__device__ __forceinline__ bool mpt_token(const Dev& d, const Buf& nxt, uint32_t j, uint32_t L, uint32_t iter,
+                                          uint32_t v, LookupF C, unsigned long long& n_skip) {
+  WordRec r;
+  if (d.geff <= 2) {  // compact view: one 32-byte load + one 4-byte load
+    const WordRecM m = d.recm[v];
+    const uint32_t kk = __ldg(d.reck + v);
+    r.a[0] = m.a0;
+    r.a[1] = m.a1;
+    r.a[2] = m.a2;
+    r.a[3] = 0.0;
+    r.Qp = m.Qp;
+    r.K[0] = (uint16_t)(kk & 0xFFFFu);
+    r.K[1] = (uint16_t)(kk >> 16);
+    r.K[2] = r.K[3] = 0;
+  } else {
+    r = d.rec[v];
+  }
   const uint32_t C1 = C(r.K[0]);
   const uint32_t C2 = d.geff >= 2 ? C(r.K[1]) : 0u;
   const uint32_t C3 = d.geff >= 3 ? C(r.K[2]) : 0u;
@@ -389,16 +410,26 @@ __device__ __forceinline__ void mpt_token(const Dev& d, const Buf& nxt, uint32_t
 #ifdef EZLDA_EXP_DOC_NOPHILOX  // diagnostic: a cheap hash instead of Philox in the doc pass
   const double u = (double)((j * 2654435761u) >> 8) * 0x1p-24;
 #else
-  const double u = philox_u(d.seed, iter, d.token_base + j);
+  const double u = philox_u_k(d.pk, iter, d.token_base + j);
 #endif
   if (mpt_skip(u, M, den)) {
     nxt.z[j] = r.K[0];
     ++n_skip;
-  } else {
-    // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
-    nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, d.c1_cap)) : kUnsampled;
-    atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
+    return false;
   }
+  // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
+  nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, d.c1_cap)) : kUnsampled;
+  return true;
+}
+
+// Flag run rid of a token that failed the MPT test (word-major run bitset, L2 resident).  The
+// lanes hold consecutive tokens of the doc: a token whose left neighbour is in the same run and
+// was flagged too leaves the atomic to it.
+__device__ __forceinline__ void flag_run(const Dev& d, bool flagged, uint32_t rid) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t prid = __shfl_up_sync(kFull, rid, 1);
+  const bool pflag = __shfl_up_sync(kFull, flagged ? 1u : 0u, 1) != 0u;
+  if (flagged && !(lane > 0 && pflag && prid == rid)) atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
 }
 
 // Per-token MPT test of one doc's tokens (shared by both doc tiers).  C(k) = D[d][k].
@@ -408,21 +439,21 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
                                                      LookupF C, unsigned long long& n_skip) {
   for (uint32_t i = start; i < L; i += stride) {
     const uint32_t j = j0 + i;
-    const uint32_t v = d.tw[j];
+    const uint32_t v = d.twr[j].x;
     const WordRec r = d.rec[v];
     const uint32_t C1 = C(r.K[0]);
     const uint32_t C2 = d.geff >= 2 ? C(r.K[1]) : 0u;
     const uint32_t C3 = d.geff >= 3 ? C(r.K[2]) : 0u;
     const double M = mpt_M(r, C1, d.alpha);
     const double den = mpt_den(r, M, C1, C2, C3, L, d.geff);
-    const double u = philox_u(d.seed, iter, d.token_base + j);
+    const double u = philox_u_k(d.pk, iter, d.token_base + j);
     if (mpt_skip(u, M, den)) {
       nxt.z[j] = r.K[0];
       ++n_skip;
     } else {
       // the sampler draws it; the marker carries C1 when K <= 32768 (see sample_batch)
       nxt.z[j] = d.zmark ? (uint16_t)(0x8000u | min(C1, d.c1_cap)) : kUnsampled;
-      const uint32_t rid = d.trid[j];
+      const uint32_t rid = d.twr[j].y;
       atomicOr(&d.flags[rid >> 5], 1u << (rid & 31u));
     }
   }
@@ -433,6 +464,11 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
 // histogram; the packed D row is emitted in topic order from the bitmap (each lane owns
 // 32-topic words: popcount prefix + set-bit walk, O(nnz + K/32) per doc) and both are
 // re-zeroed as they are read.
+// per-warp shared words of k_doc_hist: Kpad / 2 counter words + Kpad / 32 bitmap words, padded
+// to 16 bytes (the counters are re-zeroed with 16-byte stores)
+__host__ __device__ __forceinline__ uint32_t doc_hist_stride(uint32_t Kpad) {
+  return (Kpad / 2u + Kpad / 32u + 3u) & ~3u;
+}
 template <bool kSkipTest>
 #ifndef EZLDA_DOC_PF
 #define EZLDA_DOC_PF 1
@@ -446,7 +482,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t hw = d.Kpad >> 1;   // counter words per warp
   const uint32_t bw = d.Kpad >> 5;   // bitmap words per warp
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * (hw + bw);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem) + warp * doc_hist_stride(d.Kpad);
   uint32_t* bmp = hist + hw;
   for (uint32_t i = lane; i < hw + bw; i += 32) hist[i] = 0;
   __syncwarp();
@@ -487,8 +523,9 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
     for (uint32_t c = 0; c < kPre; ++c) {
       const uint32_t i = lane + 32u * c;
       pk[c] = (i < L) ? cur.z[j0 + i] : 0u;
-      pv[c] = (kSkipTest && i < L) ? d.tw[j0 + i] : 0u;
-      pr[c] = (kSkipTest && i < L) ? d.trid[j0 + i] : 0u;
+      const uint2 wr = (kSkipTest && i < L) ? d.twr[j0 + i] : make_uint2(0u, 0u);  // one 8-byte load
+      pv[c] = wr.x;
+      pr[c] = wr.y;
     }
 #pragma unroll
     for (uint32_t c = 0; c < kPre; ++c) {
@@ -507,14 +544,33 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
     if (kSkipTest) {
       auto C = [&](uint32_t k) { return (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu; };
 #pragma unroll
-      for (uint32_t c = 0; c < kPre; ++c)
-        if (lane + 32u * c < L) mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], pr[c], C, n_skip);
-      for (uint32_t i = lane + 32u * kPre; i < L; i += 32)
-        mpt_token(d, nxt, j0 + i, L, iter, d.tw[j0 + i], d.trid[j0 + i], C, n_skip);
+      for (uint32_t c = 0; c < kPre; ++c) {
+        if (32u * c >= L) break;  // warp-uniform
+        bool f = false;
+        if (lane + 32u * c < L) f = mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], C, n_skip);
+#ifndef EZLDA_EXP_DOC_NOFLAG  // diagnostic: no flag atomics (the sampler then sees no flagged run)
+        flag_run(d, f, pr[c]);
+#endif
+      }
+      for (uint32_t i0 = 32u * kPre; i0 < L; i0 += 32u) {  // warp-uniform rounds
+        const uint32_t i = i0 + lane;
+        bool f = false;
+        uint32_t rid = 0;
+        if (i < L) {
+          const uint2 wr = d.twr[j0 + i];
+          rid = wr.y;
+          f = mpt_token(d, nxt, j0 + i, L, iter, wr.x, C, n_skip);
+        }
+        flag_run(d, f, rid);
+      }
       __syncwarp();
     }
     uint32_t* Drow = d.D + dbase + kDHdr;
     uint32_t nnz = 0;
+#ifdef EZLDA_EXP_DOC_NOWALK  // diagnostic: no D-row emission (counters re-zeroed wholesale)
+    for (uint32_t i = lane; i < hw + bw; i += 32) hist[i] = 0;
+    if (false)
+#endif
     for (uint32_t base = 0; base < bw; base += 32) {
       const uint32_t wi = base + lane;
       const uint32_t b = (wi < bw) ? bmp[wi] : 0u;
@@ -530,7 +586,6 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
         const uint32_t k = wi * 32u + (__ffs(m) - 1u);
         Drow[pos++] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu, d.dt);
       }
-      for (uint32_t m = b; m; m &= m - 1u) hist[(wi * 32u + (__ffs(m) - 1u)) >> 1] = 0u;
       if (b) bmp[wi] = 0u;
       nnz += __shfl_sync(kFull, incl, 31);
     }
@@ -539,6 +594,9 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       Drow[-(int)kDHdr] = (L << 16) | nnz;
       Drow[1 - (int)kDHdr] = j0;
     }
+    __syncwarp();  // every lane's counter reads above precede the wholesale re-zeroing
+    // re-zero the counters with 16-byte stores (cheaper than a second set-bit walk)
+    for (uint32_t i = 4u * lane; i < hw; i += 128u) *reinterpret_cast<uint4*>(hist + i) = make_uint4(0u, 0u, 0u, 0u);
     n_nnz += nnz;
     __syncwarp();
   }
@@ -1126,7 +1184,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const double Sp = (double)Spi * inv_s;  // exact: Spi < 2^48
     const double M = mpt_M(rec, C1, d.alpha);
     const double Z = (M + Sp) + Qp;
-    const double u = philox_u(d.seed, iter, d.token_base + j);
+    const double u = philox_u_k(d.pk, iter, d.token_base + j);
     const double x = u * Z;
     // certification margin: m_v[k] 2^-s is within 2^-s of What'[v][k], so every fixed-point
     // prefix is within L_d 2^-s of the exact real prefix (the integer sums themselves are
@@ -1923,7 +1981,7 @@ __global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) 
     }
     const double Q = __ldg(qp + d.K - 1u);
     const double Z = S + Q;
-    const double u = philox_u(d.seed, iter, d.token_base + j);
+    const double u = philox_u_k(d.pk, iter, d.token_base + j);
     uint32_t topic = d.K - 1u;
     if (u <= S / Z) {  // S tree: first topic of the row whose prefix exceeds u Z, else the last
       const double up = u * Z;
@@ -1987,7 +2045,7 @@ __global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32
     const double Z = S + Q;
     for (uint32_t t = 0; t < len; ++t) {
       const uint32_t j = j0 + t;
-      const double u = philox_u(d.seed, iter, d.token_base + j);
+      const double u = philox_u_k(d.pk, iter, d.token_base + j);
       uint32_t topic = d.K - 1u;
       if (u <= S / Z) {
         const double up = u * Z;
@@ -2186,7 +2244,7 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
   if ((e = raise_smem(dev, (const void*)k_doc_block<false>, db))) return e;
   if ((e = raise_smem(dev, (const void*)k_doc_block<true>, db))) return e;
   if (K <= 4096) {
-    const int dh = kDocWarps * (int)(((K + 31) / 32) * 17) * 4;
+    const int dh = kDocWarps * (int)doc_hist_stride((K + 31) / 32 * 32) * 4;
     if ((e = raise_smem(dev, (const void*)k_doc_hist<false>, dh))) return e;
     if ((e = raise_smem(dev, (const void*)k_doc_hist<true>, dh))) return e;
   }
@@ -2223,7 +2281,7 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
   }
   if (n_w && d.K <= 4096) {
     const uint32_t grid = std::min<uint32_t>((n_w + kDocWarps - 1) / kDocWarps, 148u * 16u);
-    const size_t smem = (size_t)kDocWarps * (d.Kpad / 2 + d.Kpad / 32) * 4;
+    const size_t smem = (size_t)kDocWarps * doc_hist_stride(d.Kpad) * 4;
     if (skip_test)
       k_doc_hist<true><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
     else

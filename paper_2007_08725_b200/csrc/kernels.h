@@ -77,11 +77,12 @@ struct Dev {
   uint32_t grp;     // runs per sampler work claim (32; smaller at large K, sampler_group_runs)
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
+  PhiloxKeys pk;   // Philox round keys of seed (philox_keys)
   // static structure
   const uint32_t* dofs;
   const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 8 words)
   const uint32_t* tw;
-  const uint32_t* trid;
+  const uint2* twr;       // [N] (tw, run id) per doc-major token (doc pass: one 8-byte load)
   const uint32_t* run_j0;
   const uint32_t* run_dbase;
   const uint16_t* run_len;
@@ -100,6 +101,8 @@ struct Dev {
   uint32_t* D;
   uint32_t* flags;
   WordRec* rec;
+  WordRecM* recm;   // [V] a0, a1, a2, Q' of rec (doc pass, g <= 2)
+  uint32_t* reck;   // [V] K1 | K2 << 16 of rec (doc pass, g <= 2)
   double* den;    // [K] n_k + V beta
   double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
   double* inv_den;  // [K] 1 / den_k (the sampler's fixed-point heads, stage_row_warp)
