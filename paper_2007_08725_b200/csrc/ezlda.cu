@@ -1011,15 +1011,15 @@ ezlda_status fold_one(ezlda* h) {
   // DESIGN.md byte model (algorithmic bytes at payload granularity):
   //   doc pass: per token z read 2 + tw 4 ; skipped token z write 2 ; failing token trid 4 ;
   //             D rows written 4 (nnz + 4) per doc
-  //   sampler:  per active run 10 B of run table + D row 4 (nnz + 4) ; sampled token z write 2 ;
-  //             per item the staged W row (4 B x K)
+  //   sampler:  per active run 10 B of run table + D row 4 (nnz + 1) ; sampled token z write 2 ;
+  //             per armed (live) item its word's W row (4 B x K)
   //   word-prep: W rows read 4 B x Vd K (+ tail), W rebuilt 4 B x Vd K
   const double N = (double)h->N;
   const double tok_fail = N - (double)c.skip_S;
   st.model_bytes_docpass = N * (2.0 + 4.0) + (double)c.skip_S * 2.0 + tok_fail * 4.0 +
                            4.0 * ((double)c.d_nnz + 4.0 * h->Dn);
   st.model_bytes_sample = (double)c.active_runs * 10.0 + 4.0 * (double)c.drow_words + (double)c.sampled * 2.0 +
-                          (double)h->n_items * 4.0 * h->K;
+                          (double)(h->branches == 2 ? (unsigned long long)h->n_items : c.items) * 4.0 * h->K;
   st.model_bytes = st.model_bytes_docpass + st.model_bytes_sample + 2.0 * 4.0 * (double)h->Vd * h->K;
   h->last = st;
   ezlda_iter_stats& S = h->sum;

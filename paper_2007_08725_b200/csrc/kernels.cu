@@ -1459,6 +1459,7 @@ __device__ void arm_slot(const Dev& d, const Buf& cur, SlotCtl& c, unsigned char
   }
   if (d.item_act) i = d.item_act[i];  // this iteration's schedule (H4): items with a flagged run
   const uint32_t v = d.item_word[i];
+  if (lane == 0) atomicAdd(&d.ctr->items, 1ull);
   uint32_t* mrow = reinterpret_cast<uint32_t*>(sbase);
   const uint32_t mbar_s = (uint32_t)__cvta_generic_to_shared(&c.mbar);
   if (lane < 6) reinterpret_cast<uint64_t*>(&c.rec)[lane] = reinterpret_cast<const uint64_t*>(d.rec + v)[lane];

@@ -50,6 +50,7 @@ struct Counters {  // device-side per-iteration counters
   unsigned long long skip_S, skip_M, sampled, active_runs, drow_words, d_nnz;
   unsigned long long item_ctr;  // sampler work-list cursor (claimed items)
   unsigned long long exact;     // tokens redrawn on the exact fp64 path
+  unsigned long long items;     // items the sampler armed (this iteration's live items)
 };
 
 struct Dev {
