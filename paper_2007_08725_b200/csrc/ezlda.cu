@@ -911,14 +911,16 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.recm, ezl::WordRecM, h->V);
   EZ_ALLOC(h, d.reck, uint32_t, h->V);
   EZ_ALLOC(h, d.qexact, double, (size_t)h->V * d.nch);
-  // sampler heads (8 Kpad + 32 + ce bytes per word) for every word when they fit in half of
-  // the free device memory (at most 64 GiB), else for the dense words only (the other items
-  // are staged by a sampler warp)
+  // sampler heads (8 Kpad + 32 + ce bytes per word) for every word when they fit in the free
+  // device memory less a reserve (a quarter of it, at least 8 GiB, for the per-iteration
+  // scratch), else for the dense words only (the other items are staged by a sampler warp, which
+  // costs O(K) on the sampler's critical path per item)
   d.rs_bytes = ezl::head_bytes(h->K);
   if (h->branches == 3) {
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = 0;
-    const uint64_t budget = std::min<uint64_t>(64ull << 30, fr / 2);
+    const uint64_t reserve = std::max<uint64_t>(8ull << 30, fr / 4);
+    const uint64_t budget = fr > reserve ? fr - reserve : 0;
     d.Vw = ((uint64_t)h->V * d.rs_bytes <= budget) ? h->V : h->Vd;
     if (o.debug_flags & EZLDA_DEBUG_NO_TAIL_ROWS) d.Vw = h->Vd;  // tail rows staged by a sampler warp
   }

@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
   __shared__ double s_ch[kWbWarps][kWbChunk];
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t v = blockIdx.x * kWbWarps + warp;
-  if (v >= d.V || d.wtok[v + 1] == d.wtok[v]) return;  // no token of v in this shard (warp-uniform)
+  if (v >= d.Vd || d.wtok[v + 1] == d.wtok[v]) return;  // dense words only (tail: k_word_rec_tail)
   double* ch = s_ch[warp];
   // ---- pass 1: top-4 (value desc, topic asc) and an estimate of sum_k What
   Top4 t;
@@ -363,6 +363,63 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
   }
   r.Qp = d.alpha * acc;
   if (lane == 0) {
+    d.rec[v] = r;
+    d.recm[v] = WordRecM{r.a[0], r.a[1], r.a[2], r.Qp};
+    d.reck[v] = (uint32_t)r.K[0] | ((uint32_t)r.K[1] << 16);
+  }
+}
+
+// H1 records of the tail words at large K (K > 4096): one THREAD per word.  The 32 words of a
+// warp walk the topics in lockstep, so the absent-pair value What = beta / den_k (what0[k],
+// the oracle's (0 + beta) / den_k) is one broadcast load; the word's packed row is walked
+// with a cursor and only its nonzeros take the division.  Pass 1: top-4 (value desc, topic
+// asc, inserted in ascending k); pass 2: the oracle's sequential Q' sum over k != K1 with a
+// checkpoint every 32 topics.  O(K) per word, no shared memory, no idle lanes.
+__global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
+  const uint32_t Vt = d.V - d.Vd;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t v = d.Vd + t;
+  if (__all_sync(kFull, t >= Vt)) return;
+  const bool act = t < Vt && d.wtok[v + 1] != d.wtok[v];
+  const uint32_t* tr = act ? cur.Wt + d.tofs[t] : nullptr;
+  const uint32_t n = act ? cur.tnnz[t] : 0u;
+  Top4 tp;
+  top4_init(tp);
+  uint32_t e = 0, nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
+  for (uint32_t k = 0; k < d.K; ++k) {
+    double w = __ldg(d.what0 + k);
+    if (k == nk) {
+      w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
+      ++e;
+      nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
+    }
+    top4_insert(tp, w, k);
+  }
+  WordRec r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool ok = tp.v[i] >= 0.0;
+    r.a[i] = ok ? tp.v[i] : 0.0;
+    r.K[i] = ok ? (uint16_t)tp.k[i] : (uint16_t)0;
+  }
+  const uint32_t K1 = r.K[0];
+  double* qe = d.qexact + (size_t)(act ? v : 0u) * d.nch;
+  double acc = 0.0;
+  e = 0;
+  nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
+  for (uint32_t k = 0; k < d.Kpad; ++k) {
+    double w = (k < d.K) ? __ldg(d.what0 + k) : 0.0;
+    if (k == nk) {
+      w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
+      ++e;
+      nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
+    }
+    if (k == K1) w = 0.0;  // What' (Eq 6): adds +0, as the oracle skips K1
+    acc = acc + w;
+    if (act && (k & 31u) == 31u) qe[k >> 5] = acc;  // exact P_v(32 c + 31)
+  }
+  r.Qp = d.alpha * acc;
+  if (act) {
     d.rec[v] = r;
     d.recm[v] = WordRecM{r.a[0], r.a[1], r.a[2], r.Qp};
     d.reck[v] = (uint32_t)r.K[0] | ((uint32_t)r.K[1] << 16);
@@ -2267,8 +2324,9 @@ uint32_t head_bytes(uint32_t K) {  // m | scales | qfx | ce of one word (a multi
 void launch_word_prep(const Dev& d, const Buf& cur, cudaStream_t s) {
   if (d.K <= kWpSmallK) {
     k_word_prep_w<<<(d.V + kWpWarps - 1) / kWpWarps, kWpWarps * 32, word_prep_smem_bytes(d.K), s>>>(d, cur);
-  } else {
-    k_word_prep_big<<<(d.V + kWbWarps - 1) / kWbWarps, kWbWarps * 32, 0, s>>>(d, cur);
+  } else {  // dense words: warp per word (256-topic chunks); tail words: thread per word
+    if (d.Vd) k_word_prep_big<<<(d.Vd + kWbWarps - 1) / kWbWarps, kWbWarps * 32, 0, s>>>(d, cur);
+    if (d.V > d.Vd) k_word_rec_tail<<<(d.V - d.Vd + 127) / 128, 128, 0, s>>>(d, cur);
   }
 }
 
