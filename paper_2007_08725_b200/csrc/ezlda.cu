@@ -939,6 +939,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     EZ_ALLOC(h, B.z, uint16_t, N);
     EZ_ALLOC(h, B.Wd, int32_t, (size_t)h->Vd * h->K);
     EZ_ALLOC(h, B.Wt, uint32_t, h->tail_cap);
+    // (ezlda_counts copies the whole capacity; entries past tnnz are never read but stay defined)
+    if (h->tail_cap) EZ_CUDA(h, cudaMemsetAsync(B.Wt, 0, sizeof(uint32_t) * h->tail_cap, s));
     EZ_ALLOC(h, B.tnnz, uint32_t, std::max<uint32_t>(h->Vt, 1));
     EZ_ALLOC(h, B.nk, int32_t, h->K);
   }
