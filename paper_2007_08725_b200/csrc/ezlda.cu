@@ -87,38 +87,64 @@ __global__ void k_max_u16(const uint16_t* a, uint64_t n, uint32_t* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
+// D-row capacity of doc d in words: an 8-word header + min(L_d, K) entries padded to 8
+__global__ void k_rowcap(const uint32_t* L, uint32_t n, uint32_t K, uint64_t* cap) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) cap[d] = 8ull + ((min(L[d], K) + 7u) & ~7u);
+}
+__global__ void k_u64_to_u32(const uint64_t* a, uint32_t n, uint32_t* b) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (uint32_t)a[i];
+}
+// doc tiers: 1 iff L_d <= 512 (warp tier) / > 512 (block tier); key of the block tier = L_d
+__global__ void k_tier_flags(const uint32_t* L, uint32_t n, uint8_t* fw, uint8_t* fb) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) {
+    fw[d] = L[d] <= 512u ? 1u : 0u;
+    fb[d] = L[d] > 512u ? 1u : 0u;
+  }
+}
+__global__ void k_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t n, uint32_t* dst) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
 __global__ void k_hist(const uint32_t* a, uint64_t n, uint32_t* h) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     atomicAdd(&h[a[i]], 1u);
 }
 
-__global__ void k_make_keys(const uint32_t* word, const uint32_t* doc, uint32_t n, uint64_t* key, uint32_t* idx) {
+// sort key (doc << vbits) | word: a stable radix sort over the vbits + dbits significant bits
+// gives (doc, original word id, input position) order
+__global__ void k_make_keys(const uint32_t* word, const uint32_t* doc, uint32_t n, uint32_t vbits, uint64_t* key,
+                            uint32_t* idx) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    key[i] = ((uint64_t)doc[i] << 32) | word[i];
+    key[i] = ((uint64_t)doc[i] << vbits) | word[i];
     idx[i] = i;
   }
 }
 
 // tw[j] = newword[word(j)]; head[j] = 1 iff a (doc, word) run starts at j
-__global__ void k_tw_heads(const uint64_t* key, uint32_t n, const uint32_t* newword, uint32_t* tw, uint32_t* head) {
+__global__ void k_tw_heads(const uint64_t* key, uint32_t n, uint32_t vbits, const uint32_t* newword, uint32_t* tw,
+                           uint32_t* head) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) {
     const uint64_t k = key[j];
-    tw[j] = newword[(uint32_t)k];
+    tw[j] = newword[(uint32_t)(k & ((1ull << vbits) - 1ull))];
     head[j] = (j == 0 || key[j - 1] != k) ? 1u : 0u;
   }
 }
 
 // per doc-major run q (qidx = inclusive scan of heads - 1)
 __global__ void k_run_heads(const uint64_t* key, const uint32_t* head, const uint32_t* qinc, const uint32_t* tw,
-                            uint32_t n, uint32_t* q_j0, uint32_t* q_v, uint32_t* q_doc) {
+                            uint32_t n, uint32_t vbits, uint32_t* q_j0, uint32_t* q_v, uint32_t* q_doc) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n && head[j]) {
     const uint32_t q = qinc[j] - 1;
     q_j0[q] = j;
     q_v[q] = tw[j];
-    q_doc[q] = (uint32_t)(key[j] >> 32);
+    q_doc[q] = (uint32_t)(key[j] >> vbits);
   }
 }
 
@@ -202,15 +228,6 @@ __global__ void k_items(const uint32_t* r0s, uint32_t NI, uint32_t R, const uint
 // so concurrently running items sweep the D rows in the same (ascending) direction -- the L2
 // temporal locality the sampler relies on (measured: ordering runs by doc length instead cost
 // 1.7x on PubMed)
-__global__ void k_run_keys(const uint32_t* q_v, uint32_t R, uint64_t* key) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < R) key[q] = (uint64_t)q_v[q] << 16;
-}
-
-__global__ void k_key_word(const uint64_t* key, uint32_t R, uint32_t* vs) {
-  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < R) vs[r] = (uint32_t)(key[r] >> 16);
-}
 
 inline unsigned blocks(uint64_t n, unsigned t = 256) { return (unsigned)((n + t - 1) / t); }
 
@@ -312,6 +329,7 @@ struct ezlda {
       allocs.erase(it);
     }
   }
+
 };
 
 #define EZ_CUDA(h, call)                                                                                   \
@@ -574,8 +592,19 @@ ezlda_status ensure_D(ezlda* h) {
 }
 
 ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_ids, const ezlda_options& o) {
+  // EZLDA_CREATE_TIMING=1: per-phase wall time of create on stderr (stream synchronized at each mark)
+  static const bool s_tm = std::getenv("EZLDA_CREATE_TIMING") != nullptr;
+  auto t_prev = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!s_tm) return;
+    cudaStreamSynchronize(h->stream);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ezlda create] %-40s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+    t_prev = t;
+  };
   const uint32_t N = (uint32_t)h->N;
   cudaStream_t s = h->stream;
+  mark("before: inputs on device");
   // ---- inputs on device
   uint32_t *d_word, *d_doc;
   EZ_ALLOC(h, d_word, uint32_t, N);
@@ -583,6 +612,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   const cudaMemcpyKind kind = o.input_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   EZ_CUDA(h, cudaMemcpyAsync(d_word, word_ids, sizeof(uint32_t) * N, kind, s));
   EZ_CUDA(h, cudaMemcpyAsync(d_doc, doc_ids, sizeof(uint32_t) * N, kind, s));
+  mark("before: validate ids");
   // ---- validate ids
   uint32_t* d_max;
   EZ_ALLOC(h, d_max, uint32_t, 2);
@@ -594,30 +624,50 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_CUDA(h, cudaStreamSynchronize(s));
   if (mx[0] >= h->V) return h->fail(EZLDA_E_INVALID, "word id %u >= V = %u", mx[0], h->V);
   if (mx[1] >= h->Dn) return h->fail(EZLDA_E_INVALID, "doc id %u >= n_docs = %u", mx[1], h->Dn);
+  mark("before: doc lengths, word counts");
   // ---- doc lengths, word counts
-  uint32_t *d_L, *d_cnt;
-  EZ_ALLOC(h, d_L, uint32_t, h->Dn);
+  // (all per-doc tables are built on the device: doc offsets and D-row bases by scans, the
+  // doc tiers by selections; only the V word counts come to the host, for the relabelling)
+  uint32_t *d_L, *d_cnt, *d_dofs, *d_ddb;
+  uint64_t *d_cap, *d_ddb64;
+  EZ_ALLOC(h, d_L, uint32_t, h->Dn + 1);
   EZ_ALLOC(h, d_cnt, uint32_t, h->V);
-  EZ_CUDA(h, cudaMemsetAsync(d_L, 0, sizeof(uint32_t) * h->Dn, s));
+  EZ_CUDA(h, cudaMemsetAsync(d_L, 0, sizeof(uint32_t) * (h->Dn + 1), s));
   EZ_CUDA(h, cudaMemsetAsync(d_cnt, 0, sizeof(uint32_t) * h->V, s));
   k_hist<<<2368, 256, 0, s>>>(d_doc, N, d_L);
   k_hist<<<2368, 256, 0, s>>>(d_word, N, d_cnt);
-  std::vector<uint32_t> L(h->Dn), cnt_local(h->V);
-  EZ_CUDA(h, cudaMemcpyAsync(L.data(), d_L, sizeof(uint32_t) * h->Dn, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> cnt_local(h->V);
   EZ_CUDA(h, cudaMemcpyAsync(cnt_local.data(), d_cnt, sizeof(uint32_t) * h->V, cudaMemcpyDeviceToHost, s));
-  EZ_CUDA(h, cudaStreamSynchronize(s));
-  for (uint32_t d = 0; d < h->Dn; ++d)
-    if (L[d] > 65535) return h->fail(EZLDA_E_RANGE, "doc %u has %u tokens (> 65535, P:753)", d, L[d]);
-  std::vector<uint32_t> dofs(h->Dn + 1, 0);
-  for (uint32_t d = 0; d < h->Dn; ++d) dofs[d + 1] = dofs[d] + L[d];
-  // D rows: an 8-word header + min(L_d, K) entries padded to a multiple of 8 (one 32-byte
-  // sector per 8 entries; rows start sector aligned)
-  std::vector<uint32_t> ddb(h->Dn);
-  uint64_t dwords = 0;
-  for (uint32_t d = 0; d < h->Dn; ++d) {
-    ddb[d] = (uint32_t)dwords;
-    dwords += ezl::kDHdr + ((std::min<uint64_t>(L[d], h->K) + 7) & ~7ull);
+  EZ_CUDA(h, cudaMemsetAsync(d_max, 0, 4, s));
+  k_max_u32<<<1184, 256, 0, s>>>(d_L, h->Dn, d_max);
+  // doc offsets (exclusive scan of L over Dn + 1 entries: dofs[Dn] = N) and D-row bases: an
+  // 8-word header + min(L_d, K) entries padded to a multiple of 8 (one 32-byte sector per 8
+  // entries; rows start sector aligned)
+  EZ_ALLOC(h, d_dofs, uint32_t, h->Dn + 1);
+  EZ_ALLOC(h, d_cap, uint64_t, h->Dn + 1);
+  EZ_ALLOC(h, d_ddb64, uint64_t, h->Dn + 1);
+  EZ_ALLOC(h, d_ddb, uint32_t, h->Dn);
+  EZ_CUDA(h, cudaMemsetAsync(d_cap + h->Dn, 0, 8, s));
+  k_rowcap<<<blocks(h->Dn), 256, 0, s>>>(d_L, h->Dn, h->K, d_cap);
+  {
+    ezlda_status st0 = cub_call(h, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, d_L, d_dofs, (int)(h->Dn + 1), s);
+    });
+    if (st0) return st0;
+    st0 = cub_call(h, [&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, d_cap, d_ddb64, (int)(h->Dn + 1), s);
+    });
+    if (st0) return st0;
   }
+  k_u64_to_u32<<<blocks(h->Dn), 256, 0, s>>>(d_ddb64, h->Dn, d_ddb);
+  uint64_t dwords = 0;
+  uint32_t maxL = 0;
+  EZ_CUDA(h, cudaMemcpyAsync(&dwords, d_ddb64 + h->Dn, 8, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaMemcpyAsync(&maxL, d_max, 4, cudaMemcpyDeviceToHost, s));
+  EZ_CUDA(h, cudaStreamSynchronize(s));
+  h->release(d_cap);
+  h->release(d_ddb64);
+  if (maxL > 65535) return h->fail(EZLDA_E_RANGE, "a doc has %u tokens (> 65535, P:753)", maxL);
   if (dwords >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "D storage >= 2^32 words per shard");
   h->Dwords = dwords;
   // global word counts (the dense/tail split and relabelling must agree on all ranks)
@@ -643,6 +693,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   } else {
     h->N_global = N;
   }
+  mark("before: relabel words by count desc, ties by");
   // ---- relabel words by count desc, ties by id
   h->origword.resize(h->V);
   std::iota(h->origword.begin(), h->origword.end(), 0u);
@@ -665,6 +716,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->tail_cap = tofs[h->Vt];
   std::vector<uint32_t> wtok(h->V + 1, 0);
   for (uint32_t v = 0; v < h->V; ++v) wtok[v + 1] = wtok[v] + cnt_local[h->origword[v]];
+  mark("before: doc-major order: sort (doc, word, in");
   // ---- doc-major order: sort (doc, word, input position)
   uint64_t *k_in, *k_out;
   uint32_t *i_in, *i_out;
@@ -672,12 +724,13 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, k_out, uint64_t, N);
   EZ_ALLOC(h, i_in, uint32_t, N);
   EZ_ALLOC(h, i_out, uint32_t, N);
-  k_make_keys<<<blocks(N), 256, 0, s>>>(d_word, d_doc, N, k_in, i_in);
-  int dbits = 1;
+  int dbits = 1, vbits = 1;
   while (dbits < 32 && ((h->Dn - 1) >> dbits)) ++dbits;
+  while (vbits < 32 && ((h->V - 1) >> vbits)) ++vbits;
+  k_make_keys<<<blocks(N), 256, 0, s>>>(d_word, d_doc, N, (uint32_t)vbits, k_in, i_in);
   ezlda_status st;
   st = cub_call(h, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, k_in, k_out, i_in, i_out, (int)N, 0, 32 + dbits, s);
+    return cub::DeviceRadixSort::SortPairs(t, b, k_in, k_out, i_in, i_out, (int)N, 0, vbits + dbits, s);
   });
   if (st) return st;
   h->release(k_in);
@@ -685,6 +738,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(d_word);
   h->release(d_doc);
   h->perm = i_out;
+  mark("before: relabelled word per token, run heads");
   // ---- relabelled word per token, run heads
   uint32_t *d_newword, *tw, *head, *qinc;
   EZ_ALLOC(h, d_newword, uint32_t, h->V);
@@ -692,7 +746,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, tw, uint32_t, N);
   EZ_ALLOC(h, head, uint32_t, N);
   EZ_ALLOC(h, qinc, uint32_t, N);
-  k_tw_heads<<<blocks(N), 256, 0, s>>>(k_out, N, d_newword, tw, head);
+  k_tw_heads<<<blocks(N), 256, 0, s>>>(k_out, N, (uint32_t)vbits, d_newword, tw, head);
   st = cub_call(h, [&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, head, qinc, (int)N, s); });
   if (st) return st;
   uint32_t R = 0;
@@ -703,37 +757,27 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, q_j0, uint32_t, R);
   EZ_ALLOC(h, q_v, uint32_t, R);
   EZ_ALLOC(h, q_doc, uint32_t, R);
-  k_run_heads<<<blocks(N), 256, 0, s>>>(k_out, head, qinc, tw, N, q_j0, q_v, q_doc);
+  k_run_heads<<<blocks(N), 256, 0, s>>>(k_out, head, qinc, tw, N, (uint32_t)vbits, q_j0, q_v, q_doc);
   h->release(k_out);
   h->release(head);
+  mark("before: word-major run order (stable by word");
   // ---- word-major run order (stable by word => docs ascending within a word)
+  // (the relabelled word is the key: a stable radix sort over its vbits bits keeps the runs of a
+  // word in doc-major order)
   uint32_t *q_iota, *rperm, *vs;
-  uint64_t *rkey_in, *rkey_out;
   EZ_ALLOC(h, q_iota, uint32_t, R);
   EZ_ALLOC(h, rperm, uint32_t, R);
   EZ_ALLOC(h, vs, uint32_t, R);
-  EZ_ALLOC(h, rkey_in, uint64_t, R);
-  EZ_ALLOC(h, rkey_out, uint64_t, R);
   k_iota<<<blocks(R), 256, 0, s>>>(q_iota, R);
-  k_run_keys<<<blocks(R), 256, 0, s>>>(q_v, R, rkey_in);
-  int vbits = 1;
-  while (vbits < 32 && ((h->V - 1) >> vbits)) ++vbits;
   st = cub_call(h, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortPairs(t, b, rkey_in, rkey_out, q_iota, rperm, (int)R, 0, 16 + vbits, s);
+    return cub::DeviceRadixSort::SortPairs(t, b, q_v, vs, q_iota, rperm, (int)R, 0, vbits, s);
   });
   if (st) return st;
-  k_key_word<<<blocks(R), 256, 0, s>>>(rkey_out, R, vs);
-  h->release(rkey_in);
-  h->release(rkey_out);
   h->release(q_iota);
   h->release(q_v);
-  uint32_t *d_dofs, *d_ddb, *run_j0, *run_dbase, *len32, *rid_of_q;
+  uint32_t *run_j0, *run_dbase, *len32, *rid_of_q;
   uint2* twr;
   uint16_t* run_len;
-  EZ_ALLOC(h, d_dofs, uint32_t, h->Dn + 1);
-  EZ_CUDA(h, cudaMemcpyAsync(d_dofs, dofs.data(), sizeof(uint32_t) * (h->Dn + 1), cudaMemcpyHostToDevice, s));
-  EZ_ALLOC(h, d_ddb, uint32_t, h->Dn);
-  EZ_CUDA(h, cudaMemcpyAsync(d_ddb, ddb.data(), sizeof(uint32_t) * h->Dn, cudaMemcpyHostToDevice, s));
   EZ_ALLOC(h, run_j0, uint32_t, R);
   EZ_ALLOC(h, run_dbase, uint32_t, R);
   EZ_ALLOC(h, run_len, uint16_t, R);
@@ -747,6 +791,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   k_twr<<<blocks(N), 256, 0, s>>>(qinc, rid_of_q, tw, N, twr);
   h->release(qinc);
   h->release(rid_of_q);
+  mark("before: items: per word, split dense words e");
   // ---- items: per word, split dense words every split_threshold tokens
   uint32_t *wrun, *tokpre, *ihead, *r_iota, *r0s, *d_ni;
   EZ_ALLOC(h, wrun, uint32_t, h->V + 1);
@@ -795,7 +840,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(r0s);
   h->release(d_ni);
   h->release(vs);
-  if (h->multi && h->Vt) {  // ---- tail-W exchange layout (static): word-major tail runs, per-rank counts
+  if (h->multi && h->Vt) {  mark("before: tail-W exchange layout (static): wor");
+  // ---- tail-W exchange layout (static): word-major tail runs, per-rank counts
     EZ_CUDA(h, cudaMemcpyAsync(&h->rt0, wrun + h->Vd, 4, cudaMemcpyDeviceToHost, s));
     EZ_CUDA(h, cudaStreamSynchronize(s));
     EZ_ALLOC(h, h->tail_run_tok, uint32_t, std::max<uint32_t>(R - h->rt0, 1));
@@ -861,16 +907,54 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_CUDA(h, cudaMemcpyAsync(item_r0, ir0.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
   EZ_CUDA(h, cudaMemcpyAsync(item_r1, ir1.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
   EZ_CUDA(h, cudaMemcpyAsync(item_ntok, int_.data(), 4ull * NI, cudaMemcpyHostToDevice, s));
+  mark("before: doc tiers (static: L_d does not chan");
   // ---- doc tiers (static: L_d does not change)
-  std::vector<uint32_t> dw, db;
-  for (uint32_t d = 0; d < h->Dn; ++d) (L[d] <= 512 ? dw : db).push_back(d);
-  std::stable_sort(db.begin(), db.end(), [&](uint32_t a, uint32_t b) { return L[a] > L[b]; });
-  h->n_docs_w = (uint32_t)dw.size();
-  h->n_docs_b = (uint32_t)db.size();
-  EZ_ALLOC(h, h->docs_w, uint32_t, dw.size());
-  EZ_ALLOC(h, h->docs_b, uint32_t, db.size());
-  if (!dw.empty()) EZ_CUDA(h, cudaMemcpyAsync(h->docs_w, dw.data(), 4 * dw.size(), cudaMemcpyHostToDevice, s));
-  if (!db.empty()) EZ_CUDA(h, cudaMemcpyAsync(h->docs_b, db.data(), 4 * db.size(), cudaMemcpyHostToDevice, s));
+  // warp tier: docs with L_d <= 512 in doc order; block tier: the others by L_d descending
+  // (stable: ties in doc order)
+  {
+    uint8_t *fw, *fb;
+    uint32_t *d_iota, *d_nsel, *b_unsorted, *b_key, *b_key_sorted;
+    EZ_ALLOC(h, fw, uint8_t, h->Dn);
+    EZ_ALLOC(h, fb, uint8_t, h->Dn);
+    EZ_ALLOC(h, d_iota, uint32_t, h->Dn);
+    EZ_ALLOC(h, d_nsel, uint32_t, 2);
+    EZ_ALLOC(h, h->docs_w, uint32_t, h->Dn);
+    EZ_ALLOC(h, b_unsorted, uint32_t, h->Dn);
+    k_tier_flags<<<blocks(h->Dn), 256, 0, s>>>(d_L, h->Dn, fw, fb);
+    k_iota<<<blocks(h->Dn), 256, 0, s>>>(d_iota, h->Dn);
+    ezlda_status st1 = cub_call(h, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, d_iota, fw, h->docs_w, d_nsel, (int)h->Dn, s);
+    });
+    if (st1) return st1;
+    st1 = cub_call(h, [&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, d_iota, fb, b_unsorted, d_nsel + 1, (int)h->Dn, s);
+    });
+    if (st1) return st1;
+    uint32_t nsel[2];
+    EZ_CUDA(h, cudaMemcpyAsync(nsel, d_nsel, 8, cudaMemcpyDeviceToHost, s));
+    EZ_CUDA(h, cudaStreamSynchronize(s));
+    h->n_docs_w = nsel[0];
+    h->n_docs_b = nsel[1];
+    EZ_ALLOC(h, h->docs_b, uint32_t, std::max<uint32_t>(nsel[1], 1));
+    if (nsel[1]) {
+      EZ_ALLOC(h, b_key, uint32_t, nsel[1]);
+      EZ_ALLOC(h, b_key_sorted, uint32_t, nsel[1]);
+      k_gather_u32<<<blocks(nsel[1]), 256, 0, s>>>(d_L, b_unsorted, nsel[1], b_key);
+      st1 = cub_call(h, [&](void* t, size_t& b) {
+        return cub::DeviceRadixSort::SortPairsDescending(t, b, b_key, b_key_sorted, b_unsorted, h->docs_b,
+                                                         (int)nsel[1], 0, 16, s);
+      });
+      if (st1) return st1;
+      h->release(b_key);
+      h->release(b_key_sorted);
+    }
+    h->release(fw);
+    h->release(fb);
+    h->release(d_iota);
+    h->release(d_nsel);
+    h->release(b_unsorted);
+  }
+  mark("before: remaining state");
   // ---- remaining state
   uint32_t *d_tofs, *d_wtok;
   EZ_ALLOC(h, d_tofs, uint32_t, h->Vt + 1);
@@ -965,12 +1049,14 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     EZ_CUDA(h, cudaMemsetAsync(d.hist_scratch, 0, nh * sizeof(uint32_t), s));
     if (d.qfx_global) EZ_ALLOC(h, d.qfx_scratch, uint32_t, (size_t)d.sampler_grid * d.nslots * d.Kpad);
   }
+  mark("before: iteration 0");
   // ---- iteration 0
   h->cur = 0;
   ezl::launch_init_topics(d, h->buf[0].z, s);
   EZ_CUDA(h, cudaGetLastError());
   if ((st = rebuild_counts(h))) return st;
   EZ_CUDA(h, cudaStreamSynchronize(s));
+  mark("end (iteration 0)");
   h->iteration = 0;
   return EZLDA_OK;
 }
