@@ -1953,22 +1953,29 @@ __global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double
     chunk_prefix(row, d.nch, T, CP);
     const double Qfull = d.alpha * CP[d.nch];
     const double Kalpha = (double)d.K * d.alpha;
+    // lane per run: the run's packed D row walked sector by sector (8 entries per 32-byte load,
+    // zero padded) with the fp64 products summed in the lane (any order is within the 1e-10
+    // the LLPT parity asks: ~nnz ulps)
     double acc = 0.0;
-    for (uint32_t r = r0 + warp; r < r1; r += kLlptWarps) {
+    (void)lane;
+    for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) {
       const uint32_t dbase = d.run_dbase[r], len = d.run_len[r];
-      const uint32_t hdr = d.D[dbase];
+      const uint32_t hdr = __ldg(d.D + dbase);
       const uint32_t L = hdr >> 16, nnz = hdr & 0xFFFFu;
       const uint32_t* Drow = d.D + dbase + kDHdr;
-      double carry = 0.0;
-      for (uint32_t c = 0; c * 32u < nnz; ++c) {
-        const uint32_t i = c * 32u + lane;
-        const uint32_t e = (i < nnz) ? Drow[i] : 0u;
-        const double w = (i < nnz) ? (double)(e & 0xFFFFu) * row[d_topic(e, d.dt)] : 0.0;
-        carry = carry + __shfl_sync(kFull, warp_incl_scan(w), 31);
+      double S = 0.0;
+      for (uint32_t e0 = 0; e0 < nnz; e0 += 8u) {
+        uint4 qa, qb;
+        ldg256(Drow + e0, qa, qb);
+        const uint32_t ev[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)  // padding entries are 0: count 0 adds +0
+          S = S + u2d(ev[i] & 0xFFFFu) * row[d_topic(ev[i], d.dt)];
       }
-      const double p = (carry + Qfull) / ((double)L + Kalpha);
+      const double p = (S + Qfull) / ((double)L + Kalpha);
       acc = acc + (double)len * log2(p);
     }
+    acc = warp_sum(acc);
     if (lane == 0) s_acc[warp] = acc;
     __syncthreads();
     if (tid == 0) {
