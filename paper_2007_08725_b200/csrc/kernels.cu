@@ -938,6 +938,37 @@ __device__ __forceinline__ uint32_t tail_count(const uint32_t* E, uint32_t nnz, 
   return packed_count(E, nnz, k, 16u);
 }
 
+// The oracle's per-token draw (SURVEY 8(c) steps 4-8) in fp64 with its summation orders:
+// S' = ascending sequential sum over the row's topics != K1 of D[d][k] What[v][k], Z = (M +
+// S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fast
+// path could not certify its decision.
+// W[v][k] for the ascending topics of a walk over a D row: dense rows by index, tail rows by a
+// cursor merged along the sorted packed row (one pass instead of a binary search per entry)
+struct WCursor {
+  const int32_t* wr;
+  const uint32_t* tr;
+  uint32_t tn, te;
+  __device__ __forceinline__ uint32_t at(uint32_t k) {
+    if (wr) return (uint32_t)wr[k];
+    while (te < tn && (tr[te] >> 16) < k) ++te;
+    return (te < tn && (tr[te] >> 16) == k) ? (tr[te] & 0xFFFFu) : 0u;
+  }
+};
+__device__ __forceinline__ WCursor wcursor(const Dev& d, const Buf& cur, uint32_t v) {
+  WCursor c;
+  if (v < d.Vd) {
+    c.wr = cur.Wd + (size_t)v * d.K;
+    c.tr = nullptr;
+    c.tn = 0;
+  } else {
+    c.wr = nullptr;
+    c.tr = cur.Wt + d.tofs[v - d.Vd];
+    c.tn = cur.tnnz[v - d.Vd];
+  }
+  c.te = 0;
+  return c;
+}
+
 // What[v][k] in fp64 exactly as word-prep / the oracle form it: (W[v][k] + beta) / den_k.
 __device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint32_t v, uint32_t k) {
   uint32_t c;
@@ -945,25 +976,31 @@ __device__ __forceinline__ double what_exact(const Dev& d, const Buf& cur, uint3
     c = (uint32_t)cur.Wd[(size_t)v * d.K + k];
   } else {
     const uint32_t t = v - d.Vd;
-    const uint32_t* tr = cur.Wt + d.tofs[t];
-    c = tail_count(tr, cur.tnnz[t], k);
+    c = tail_count(cur.Wt + d.tofs[t], cur.tnnz[t], k);
   }
   return ((double)c + d.beta) / d.den[k];
 }
 
-// The oracle's per-token draw (SURVEY 8(c) steps 4-8) in fp64 with its summation orders:
-// S' = ascending sequential sum over the row's topics != K1 of D[d][k] What[v][k], Z = (M +
-// S') + Q', x = u Z, [M | S' | Q'] descents.  Used for the (rare) tokens whose fast
-// path could not certify its decision.
+// kMerge (large K, where tail words carry a large share of the exact redraws): W[v][k] along the
+// D row by a cursor merged with the packed tail row; else a binary search per entry (fewer live
+// registers in the sampler's token loop)
+template <bool kMerge>
 __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const WordRec& rec, const uint32_t* E,
                                uint32_t nnz, double M, double u, bool& hitM) {
   const uint32_t K1 = rec.K[0];
   double Sp = 0.0;
-#pragma unroll 4
-  for (uint32_t e = 0; e < nnz; ++e) {
-    const uint32_t w = __ldg(E + e);
-    const uint32_t k = d_topic(w, d.dt);
-    if (k != K1) Sp = Sp + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
+  {
+    WCursor wc = wcursor(d, cur, v);
+    for (uint32_t e = 0; e < nnz; ++e) {
+      const uint32_t w = __ldg(E + e);
+      const uint32_t k = d_topic(w, d.dt);
+      if (kMerge) {
+        const uint32_t c = wc.at(k);
+        if (k != K1) Sp = Sp + (double)(w & 0xFFFFu) * (((double)c + d.beta) / d.den[k]);
+      } else if (k != K1) {
+        Sp = Sp + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
+      }
+    }
   }
   const double Z = (M + Sp) + rec.Qp;
   const double x = u * Z;
@@ -976,11 +1013,13 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
     const double y = x - M;
     double acc = 0.0;
     uint32_t last = K1;
+    WCursor wc = wcursor(d, cur, v);
     for (uint32_t e = 0; e < nnz; ++e) {
       const uint32_t w = __ldg(E + e);
       const uint32_t k = d_topic(w, d.dt);
+      const uint32_t c = kMerge ? wc.at(k) : 0u;
       if (k == K1) continue;
-      acc = acc + (double)(w & 0xFFFFu) * what_exact(d, cur, v, k);
+      acc = acc + (double)(w & 0xFFFFu) * (kMerge ? (((double)c + d.beta) / d.den[k]) : what_exact(d, cur, v, k));
       last = k;
       if (acc > y) return k;
     }
@@ -1346,7 +1385,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
       }
     }
     if (topic == 0xFFFFFFFFu) {
-      topic = exact_draw(d, cur, v, rec, E, s_nnz, M, u, hit);
+      topic = exact_draw<(kSub == 16u)>(d, cur, v, rec, E, s_nnz, M, u, hit);
       rc.exact += 1;
     }
     if (hit) rc.hitM += 1;
