@@ -109,6 +109,15 @@ __global__ void k_gather_u32(const uint32_t* src, const uint32_t* idx, uint32_t 
   if (i < n) dst[i] = src[idx[i]];
 }
 
+// keys / topics of the absent-pair order (positive doubles order like their bit patterns)
+__global__ void k_w0_keys(const double* what0, uint32_t K, unsigned long long* key, uint32_t* topic) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < K) {
+    key[k] = (unsigned long long)__double_as_longlong(what0[k]);
+    topic[k] = k;
+  }
+}
+
 __global__ void k_hist(const uint32_t* a, uint64_t n, uint32_t* h) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     atomicAdd(&h[a[i]], 1u);
@@ -291,6 +300,10 @@ struct ezlda {
   // H4 per-iteration schedule: CUB select of the live items (static order preserved)
   uint32_t* item_iota = nullptr;
   uint32_t* item_act = nullptr;
+  unsigned long long *w0_key_in = nullptr, *w0_key_out = nullptr;  // absent-pair order (large K)
+  uint32_t* w0_top_in = nullptr;
+  unsigned char* w0_tmp = nullptr;
+  size_t w0_tmp_bytes = 0;
   uint32_t* n_act = nullptr;
   void* sel_tmp = nullptr;
   size_t sel_tmp_bytes = 0;
@@ -1017,6 +1030,16 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.den, double, h->K);
   EZ_ALLOC(h, d.what0, double, h->K);
   EZ_ALLOC(h, d.inv_den, double, h->K);
+  if (h->K > 4096u && h->Vt && h->branches == 3) {  // absent-pair order of the tail records
+    EZ_ALLOC(h, d.w0ord, uint32_t, h->K);
+    EZ_ALLOC(h, h->w0_key_in, unsigned long long, h->K);
+    EZ_ALLOC(h, h->w0_key_out, unsigned long long, h->K);
+    EZ_ALLOC(h, h->w0_top_in, uint32_t, h->K);
+    h->w0_tmp_bytes = 0;
+    EZ_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, h->w0_tmp_bytes, h->w0_key_in, h->w0_key_out,
+                                                         h->w0_top_in, d.w0ord, (int)h->K, 0, 64, s));
+    EZ_ALLOC(h, h->w0_tmp, unsigned char, std::max<size_t>(h->w0_tmp_bytes, 1));
+  }
   EZ_ALLOC(h, d.ctr, ezl::Counters, 1);
   for (int b = 0; b < 2; ++b) {
     Buf& B = h->buf[b];
@@ -1270,6 +1293,11 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
       if (!h->multi) ezl::launch_nk(h->dev, nxt, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[3], s));
     } else {
+      if (h->dev.w0ord) {  // the iteration's absent-pair order (stable radix sort: ties by topic asc)
+        k_w0_keys<<<blocks(h->K), 256, 0, s>>>(h->dev.what0, h->K, h->w0_key_in, h->w0_top_in);
+        EZ_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->w0_tmp, h->w0_tmp_bytes, h->w0_key_in, h->w0_key_out,
+                                                             h->w0_top_in, h->dev.w0ord, (int)h->K, 0, 64, s));
+      }
       ezl::launch_word_prep(h->dev, cur, s);
       if (h->timing) EZ_CUDA(h, cudaEventRecord(ev[1], s));
       ezl::launch_doc_pass(h->dev, cur, nxt, h->docs_w, h->n_docs_w, h->docs_b, h->n_docs_b, i, true, s);

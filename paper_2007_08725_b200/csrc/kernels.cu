@@ -369,33 +369,51 @@ __global__ void __launch_bounds__(kWbWarps * 32) k_word_prep_big(Dev d, Buf cur)
   }
 }
 
-// H1 records of the tail words at large K (K > 4096): one THREAD per word.  The 32 words of a
-// warp walk the topics in lockstep, so the absent-pair value What = beta / den_k (what0[k],
-// the oracle's (0 + beta) / den_k) is one broadcast load; the word's packed row is walked
-// with a cursor and only its nonzeros take the division.  Pass 1: top-4 (value desc, topic
-// asc, inserted in ascending k); pass 2: the oracle's sequential Q' sum over k != K1 with a
-// checkpoint every 32 topics.  O(K) per word, no shared memory, no idle lanes.
+// H1 records of the tail words at large K (K > 4096): one THREAD per word.
+//   Top-4: the word's nonzeros (What = (W + beta) / den_k) and its four best ABSENT topics,
+//     whose value What = beta / den_k (what0[k], the oracle's (0 + beta) / den_k) is the same
+//     for every tail word: they are the first four topics of the iteration's global order of
+//     what0 (value desc, topic asc: d.w0ord, sorted once per iteration) that are not in the
+//     word's row.  Any later absent topic ranks below them, so the top-4 is exact.
+//   Q': the oracle's sequential sum over k != K1 in ascending k, with a checkpoint every 32
+//     topics: the 128 words of a block walk the topics in lockstep, what0 staged through
+//     shared memory in chunks (one broadcast read per topic), the word's packed row merged
+//     with a cursor (only its nonzeros take the division).
+constexpr uint32_t kTailChunk = 2048;  // what0 doubles per shared-memory chunk
+__device__ __forceinline__ bool row_has(const uint32_t* tr, uint32_t n, uint32_t k) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((tr[mid] >> 16) < k) lo = mid + 1u; else hi = mid;
+  }
+  return lo < n && (tr[lo] >> 16) == k;
+}
 __global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
+  __shared__ double s_w0[kTailChunk];
   const uint32_t Vt = d.V - d.Vd;
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t v = d.Vd + t;
-  if (__all_sync(kFull, t >= Vt)) return;
   const bool act = t < Vt && d.wtok[v + 1] != d.wtok[v];
   const uint32_t* tr = act ? cur.Wt + d.tofs[t] : nullptr;
   const uint32_t n = act ? cur.tnnz[t] : 0u;
   Top4 tp;
   top4_init(tp);
-  uint32_t e = 0, nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
-  for (uint32_t k = 0; k < d.K; ++k) {
-    double w = __ldg(d.what0 + k);
-    if (k == nk) {
-      w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
-      ++e;
-      nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
-    }
-    top4_insert(tp, w, k);
-  }
   WordRec r;
+  if (act) {
+    for (uint32_t e = 0; e < n; ++e) {
+      const uint32_t p = tr[e];
+      const uint32_t k = p >> 16;
+      top4_insert(tp, ((double)(p & 0xFFFFu) + d.beta) / d.den[k], k);
+    }
+    uint32_t found = 0;
+    for (uint32_t i = 0; found < 4u && i < d.K; ++i) {
+      const uint32_t k = __ldg(d.w0ord + i);
+      if (!row_has(tr, n, k)) {
+        top4_insert(tp, __ldg(d.what0 + k), k);
+        ++found;
+      }
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const bool ok = tp.v[i] >= 0.0;
@@ -405,18 +423,24 @@ __global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
   const uint32_t K1 = r.K[0];
   double* qe = d.qexact + (size_t)(act ? v : 0u) * d.nch;
   double acc = 0.0;
-  e = 0;
-  nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
-  for (uint32_t k = 0; k < d.Kpad; ++k) {
-    double w = (k < d.K) ? __ldg(d.what0 + k) : 0.0;
-    if (k == nk) {
-      w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
-      ++e;
-      nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
+  uint32_t e = 0, nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
+  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += kTailChunk) {  // (every thread of the block: barriers)
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kTailChunk; i += blockDim.x)
+      s_w0[i] = (c0 + i < d.K) ? __ldg(d.what0 + c0 + i) : 0.0;
+    __syncthreads();
+    const uint32_t cend = min(c0 + kTailChunk, d.Kpad);
+    for (uint32_t k = c0; k < cend; ++k) {
+      double w = s_w0[k - c0];
+      if (k == nk) {
+        w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
+        ++e;
+        nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
+      }
+      if (k == K1) w = 0.0;  // What' (Eq 6): adds +0, as the oracle skips K1
+      acc = acc + w;
+      if (act && (k & 31u) == 31u) qe[k >> 5] = acc;  // exact P_v(32 c + 31)
     }
-    if (k == K1) w = 0.0;  // What' (Eq 6): adds +0, as the oracle skips K1
-    acc = acc + w;
-    if (act && (k & 31u) == 31u) qe[k >> 5] = acc;  // exact P_v(32 c + 31)
   }
   r.Qp = d.alpha * acc;
   if (act) {
