@@ -1508,35 +1508,56 @@ __device__ void stage_row_warp(const Dev& d, const Buf& cur, uint32_t v, const W
     }
     __syncwarp();
   }
+  // 128 topics per step, four consecutive topics per lane: local prefix of the four, one warp
+  // scan of the lane totals (exclusive prefix by a shifted read, no subtraction), 16-byte m /
+  // qfx stores; the chunk ends ce[c] = qfx[32 c + 31] fall on lanes 7, 15, 23, 31
   double carry = 0.0;
-  constexpr uint32_t kU = 4;  // chunks in flight per step
-  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += 32u * kU) {
-    uint32_t cnt[kU];
-    double id[kU];
+  for (uint32_t c0 = 0; c0 < d.Kpad; c0 += 128u) {
+    const uint32_t kb = c0 + 4u * lane;  // a multiple of 4; Kpad too: all four in or all out
+    const bool in4 = kb < d.Kpad;
+    double w[4];
+    if (in4) {
+      uint32_t cnt[4];
+      if (dense) {
 #pragma unroll
-    for (uint32_t u = 0; u < kU; ++u) {
-      const uint32_t k = c0 + 32u * u + lane;
-      const bool in = k < d.K;
-      cnt[u] = in ? (dense ? (uint32_t)__ldg(wr + k) : m[k]) : 0u;
-      id[u] = in ? __ldg(d.inv_den + k) : 0.0;
-    }
-#pragma unroll
-    for (uint32_t u = 0; u < kU; ++u) {
-      const uint32_t k = c0 + 32u * u + lane;
-      if (k >= d.Kpad) break;  // warp-uniform (Kpad is a multiple of 32)
-      const double w = (k < d.K && k != K1) ? ((double)cnt[u] + d.beta) * id[u] : 0.0;
-      m[k] = __double2uint_rn(fmin(w * two_s, 4294967295.0));
-      double x = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(kFull, x, o);
-        if (lane >= (uint32_t)o) x = x + y;
+        for (int i = 0; i < 4; ++i) cnt[i] = (kb + i < d.K) ? (uint32_t)__ldg(wr + kb + i) : 0u;
+      } else {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(m + kb);
+        cnt[0] = c4.x; cnt[1] = c4.y; cnt[2] = c4.z; cnt[3] = c4.w;
       }
-      const uint32_t q = __double2uint_rn(fmin(d.alpha * (carry + x) * two_t, 4294967295.0));
-      qfx[k] = q;
-      if (lane == 31u) ce[k >> 5] = q;
-      carry = carry + __shfl_sync(kFull, x, 31);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t k = kb + i;
+        w[i] = (k < d.K && k != K1) ? ((double)cnt[i] + d.beta) * __ldg(d.inv_den + k) : 0.0;
+      }
+      uint4 mm;
+      mm.x = __double2uint_rn(fmin(w[0] * two_s, 4294967295.0));
+      mm.y = __double2uint_rn(fmin(w[1] * two_s, 4294967295.0));
+      mm.z = __double2uint_rn(fmin(w[2] * two_s, 4294967295.0));
+      mm.w = __double2uint_rn(fmin(w[3] * two_s, 4294967295.0));
+      *reinterpret_cast<uint4*>(m + kb) = mm;
+    } else {
+      w[0] = w[1] = w[2] = w[3] = 0.0;
     }
+    const double p0 = w[0], p1 = p0 + w[1], p2 = p1 + w[2], p3 = p2 + w[3];
+    double incl = p3;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= (uint32_t)o) incl = incl + y;
+    }
+    const double prev = __shfl_up_sync(kFull, incl, 1);
+    const double base = carry + (lane ? prev : 0.0);
+    if (in4) {
+      uint4 q4;
+      q4.x = __double2uint_rn(fmin(d.alpha * (base + p0) * two_t, 4294967295.0));
+      q4.y = __double2uint_rn(fmin(d.alpha * (base + p1) * two_t, 4294967295.0));
+      q4.z = __double2uint_rn(fmin(d.alpha * (base + p2) * two_t, 4294967295.0));
+      q4.w = __double2uint_rn(fmin(d.alpha * (base + p3) * two_t, 4294967295.0));
+      *reinterpret_cast<uint4*>(qfx + kb) = q4;
+      if ((lane & 7u) == 7u) ce[(kb + 3u) >> 5] = q4.w;
+    }
+    carry = carry + __shfl_sync(kFull, incl, 31);
   }
   for (uint32_t c = d.nch + lane; c < ce_words(d.Kpad); c += 32u) ce[c] = 0xFFFFFFFFu;
   if (lane == 0) {
