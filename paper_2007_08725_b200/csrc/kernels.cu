@@ -1308,11 +1308,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const double x = u * Z;
     // certification margin: m_v[k] = rint(What'~ 2^s) with What'~ within 2^-52 relative of
     // What'[v][k] (the reciprocal), so |m 2^-s - What'| <= (1/2 + 2^-20) 2^-s and every
-    // fixed-point prefix (exact integer sums) is within delta = 0.500001 L_d 2^-s of the exact
+    // fixed-point prefix (exact integer sums) is within delta = 0.500001 (L_d - C1) 2^-s of the exact
     // real prefix; x and y inherit it at most twice (2 delta); the oracle's own sequential fp64
     // sums of nnz terms are within nnz 2^-53 of exact (1.2e-16 nnz Z), and 4e-15 Z covers the
     // roundings of M, Z and x
-    const double mg = 1.000002 * (double)s_L * inv_s + (4e-15 + 1.2e-16 * (double)s_nnz) * Z;
+    // (the K1 entry of m is 0, exact: only the other L_d - C1 counts carry the error)
+    const double mg = 1.000002 * (double)(s_L - C1) * inv_s + (4e-15 + 1.2e-16 * (double)s_nnz) * Z;
     uint32_t topic = 0xFFFFFFFFu;
     bool hit = false;
     if (!d.exact_all && fabs(x - M) > mg && fabs(x - (M + Sp)) > mg) {
