@@ -111,8 +111,9 @@ typedef struct {
  * words only, so every tail-word item is staged by a sampler warp (the path large V x K
  * shards take when the rows do not fit).  C1_LOOKUP: the doc pass never carries C1 in the
  * z^i marker, so every sampled token looks C1 up in the packed D row (the path of
- * C1 >= 0x7FFF). */
-enum { EZLDA_DEBUG_NO_TAIL_ROWS = 1u, EZLDA_DEBUG_C1_LOOKUP = 2u };
+ * C1 >= 0x7FFF).  DPERM_ON / DPERM_OFF: force the sector-interleaved D-row layout on / off
+ * (by default it is used when K <= 4096 and the shard averages >= 192 tokens per doc). */
+enum { EZLDA_DEBUG_NO_TAIL_ROWS = 1u, EZLDA_DEBUG_C1_LOOKUP = 2u, EZLDA_DEBUG_DPERM_ON = 4u, EZLDA_DEBUG_DPERM_OFF = 8u };
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL
  * to query nnz (row_ptr may also be NULL then).  row_ptr has rows+1 entries. */

@@ -88,13 +88,29 @@ __global__ void k_max_u16(const uint16_t* a, uint64_t n, uint32_t* out) {
 }
 
 // D-row capacity of doc d in words: an 8-word header + min(L_d, K) entries padded to 8
-__global__ void k_rowcap(const uint32_t* L, uint32_t n, uint32_t K, uint64_t* cap) {
-  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
-  if (d < n) cap[d] = 8ull + ((min(L[d], K) + 7u) & ~7u);
+// Sector-interleaved D rows (kernels.h d_phys) when K <= 4096 and the docs are long: every row
+// then pays a header line of its own (the entries start on a line), which costs more L2 / DRAM
+// than the coalesced phase-B loads save when rows are short (A/B, profiles/r02/ab_dperm.log:
+// NYTimes-shaped (332 tokens per doc) sampler 19.8 -> 18.4 ms, PubMed-shaped (90) 73.0 -> 75.0 ms
+// with DRAM reads 187 -> 235 GB).  debug_flags force it on / off.
+#ifndef EZLDA_DPERM_MIN_MEAN_L
+#define EZLDA_DPERM_MIN_MEAN_L 192
+#endif
+static uint32_t dperm_of(uint32_t K, uint64_t N, uint32_t Dn, uint32_t flags) {
+  if (!ezl::kDPermOn || K > ezl::kDPermMaxK || (flags & EZLDA_DEBUG_DPERM_OFF)) return 0u;
+  if (flags & EZLDA_DEBUG_DPERM_ON) return 1u;
+  return (Dn && N >= (uint64_t)EZLDA_DPERM_MIN_MEAN_L * Dn) ? 1u : 0u;
 }
-__global__ void k_u64_to_u32(const uint64_t* a, uint32_t n, uint32_t* b) {
+// D-row capacity: an 8-word header + min(L_d, K) entries padded to a multiple of 8 (one 32-byte
+// sector per 8 entries); sector-interleaved rows (perm): whole 64-entry blocks, and the header
+// sector preceded by 24 unused words so that every row's entries start on a 128-byte line
+__global__ void k_rowcap(const uint32_t* L, uint32_t n, uint32_t K, uint32_t perm, uint64_t* cap) {
+  const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) cap[d] = perm ? 32ull + ((min(L[d], K) + 63u) & ~63u) : 8ull + ((min(L[d], K) + 7u) & ~7u);
+}
+__global__ void k_u64_to_u32(const uint64_t* a, uint32_t n, uint32_t add, uint32_t* b) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) b[i] = (uint32_t)a[i];
+  if (i < n) b[i] = (uint32_t)a[i] + add;
 }
 // doc tiers: 1 iff L_d <= 512 (warp tier) / > 512 (block tier); key of the block tier = L_d
 __global__ void k_tier_flags(const uint32_t* L, uint32_t n, uint8_t* fw, uint8_t* fb) {
@@ -258,6 +274,7 @@ struct ezlda {
   uint32_t n_items = 0, n_docs_w = 0, n_docs_b = 0;
   uint64_t tail_cap = 0;
   uint64_t Dwords = 0;
+  uint32_t dperm = 0;                 // sector-interleaved D rows (dperm_of)
   uint32_t cut_min = 0;
   double alpha = 0, beta = 0;
   uint64_t seed = 0;
@@ -555,6 +572,7 @@ void fill_dev(ezlda* h) {
   d.Vd = h->Vd;
   ezl::seg_config(h->K, &d.segw, &d.segsub, &d.segfb);
   d.dt = ezl::d_shift(h->K);
+  d.dperm = h->dperm;
   d.grp = ezl::sampler_group_runs(h->K);
   d.zmark = h->K <= 32768u ? 1u : 0u;
   d.c1_cap = (h->debug_flags & EZLDA_DEBUG_C1_LOOKUP) ? 0u : 0x7FFFu;
@@ -661,7 +679,9 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d_ddb64, uint64_t, h->Dn + 1);
   EZ_ALLOC(h, d_ddb, uint32_t, h->Dn);
   EZ_CUDA(h, cudaMemsetAsync(d_cap + h->Dn, 0, 8, s));
-  k_rowcap<<<blocks(h->Dn), 256, 0, s>>>(d_L, h->Dn, h->K, d_cap);
+  const uint32_t dperm = dperm_of(h->K, N, h->Dn, h->debug_flags);
+  h->dperm = dperm;
+  k_rowcap<<<blocks(h->Dn), 256, 0, s>>>(d_L, h->Dn, h->K, dperm, d_cap);
   {
     ezlda_status st0 = cub_call(h, [&](void* t, size_t& b) {
       return cub::DeviceScan::ExclusiveSum(t, b, d_L, d_dofs, (int)(h->Dn + 1), s);
@@ -672,7 +692,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     });
     if (st0) return st0;
   }
-  k_u64_to_u32<<<blocks(h->Dn), 256, 0, s>>>(d_ddb64, h->Dn, d_ddb);
+  // (perm: bases 24 mod 32 words, so that the entries after the 8-word header start on a line)
+  k_u64_to_u32<<<blocks(h->Dn), 256, 0, s>>>(d_ddb64, h->Dn, dperm ? 24u : 0u, d_ddb);
   uint64_t dwords = 0;
   uint32_t maxL = 0;
   EZ_CUDA(h, cudaMemcpyAsync(&dwords, d_ddb64 + h->Dn, 8, cudaMemcpyDeviceToHost, s));
@@ -681,8 +702,8 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   h->release(d_cap);
   h->release(d_ddb64);
   if (maxL > 65535) return h->fail(EZLDA_E_RANGE, "a doc has %u tokens (> 65535, P:753)", maxL);
-  if (dwords >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "D storage >= 2^32 words per shard");
-  h->Dwords = dwords;
+  if (dwords + 24u >= (1ull << 32)) return h->fail(EZLDA_E_RANGE, "D storage >= 2^32 words per shard");
+  h->Dwords = dwords + (dperm ? 24u : 0u);
   // global word counts (the dense/tail split and relabelling must agree on all ranks)
   std::vector<uint64_t> cnt(h->V);
   for (uint32_t v = 0; v < h->V; ++v) cnt[v] = cnt_local[v];
@@ -1419,7 +1440,7 @@ ezlda_status ezlda_counts(ezlda* h, uint16_t* topics, int32_t* n_k, ezlda_csr* W
       const uint32_t base = ddb[d];
       const uint32_t n = (dofs[d + 1] > dofs[d]) ? (Dh[base] & 0xFFFFu) : 0u;
       for (uint32_t e = 0; e < n; ++e) {
-        const uint32_t p = Dh[base + ezl::kDHdr + e];
+        const uint32_t p = Dh[base + ezl::kDHdr + ezl::d_at(h->dev.dperm, e)];
         if (fill) {
           if (nnz >= D->nnz) return h->fail(EZLDA_E_INVALID, "D csr capacity too small");
           D->col[nnz] = (uint16_t)ezl::d_topic(p, h->dev.dt);

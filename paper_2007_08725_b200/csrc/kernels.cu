@@ -122,7 +122,7 @@ __device__ __forceinline__ void top4_insert(Top4& t, double v, uint32_t k) {
 // Block-wide ordered compaction: out[pos] = (k << shift) | hist[k] for every k < K with
 // hist[k] > 0, ascending k.  Returns nnz in all threads.
 __device__ uint32_t block_compact(const uint32_t* hist, uint32_t K, uint32_t* out, uint32_t* s_wsum,
-                                  uint32_t* s_run, uint32_t shift) {
+                                  uint32_t* s_run, uint32_t shift, uint32_t perm = 0u) {
   const uint32_t tid = threadIdx.x, nt = blockDim.x, lane = tid & 31u, warp = tid >> 5, nw = nt >> 5;
   if (tid == 0) *s_run = 0;
   __syncthreads();
@@ -136,7 +136,7 @@ __device__ uint32_t block_compact(const uint32_t* hist, uint32_t K, uint32_t* ou
     uint32_t before = 0;
     for (uint32_t w = 0; w < warp; ++w) before += s_wsum[w];
     const uint32_t pos = *s_run + before + __popc(m & lanemask_lt());
-    if (f) out[pos] = (k << shift) | c;
+    if (f) out[d_at(perm, pos)] = (k << shift) | c;
     __syncthreads();
     if (tid == 0) {
       uint32_t tot = 0;
@@ -665,12 +665,12 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       uint32_t pos = nnz + incl - cnt;
       for (uint32_t m = b; m; m &= m - 1u) {
         const uint32_t k = wi * 32u + (__ffs(m) - 1u);
-        Drow[pos++] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu, d.dt);
+        Drow[d_at(d.dperm, pos++)] = d_entry(k, (hist[k >> 1] >> ((k & 1u) << 4)) & 0xFFFFu, d.dt);
       }
       if (b) bmp[wi] = 0u;
       nnz += __shfl_sync(kFull, incl, 31);
     }
-    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[p] = 0u;  // pad to 8
+    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[d_at(d.dperm, p)] = 0u;  // pad to 8
     if (lane == 0) {
       Drow[-(int)kDHdr] = (L << 16) | nnz;
       Drow[1 - (int)kDHdr] = j0;
@@ -783,8 +783,8 @@ __global__ void __launch_bounds__(256) k_doc_block(Dev d, Buf cur, Buf nxt, cons
   for (uint32_t i = tid; i < L; i += nt) atomicAdd(&hist[cur.z[j0 + i]], 1u);
   __syncthreads();
   uint32_t* Drow = d.D + dbase;
-  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run, d.dt);
-  for (uint32_t p = nnz + tid; p < ((nnz + 7u) & ~7u); p += nt) Drow[kDHdr + p] = 0u;  // pad to 8
+  const uint32_t nnz = block_compact(hist, d.K, Drow + kDHdr, s_wsum, &s_run, d.dt, d.dperm);
+  for (uint32_t p = nnz + tid; p < ((nnz + 7u) & ~7u); p += nt) Drow[kDHdr + d_at(d.dperm, p)] = 0u;  // pad to 8
   if (tid == 0) {
     Drow[0] = (L << 16) | nnz;
     Drow[1] = j0;
@@ -835,6 +835,16 @@ __device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over
 #endif
 #ifndef EZLDA_B_PF
 #define EZLDA_B_PF 1
+#endif
+#ifndef EZLDA_QSWZ
+#define EZLDA_QSWZ 1
+#endif
+// The fixed-point Q' table is stored XOR-swizzled within each 32-topic chunk (topic i at
+// i ^ (chunk & 31)): the lanes of a warp search different chunks in step, so an unswizzled
+// table sends them all to the same bank (e.g. every lane's first probe is entry 15 of its chunk)
+__device__ __forceinline__ uint32_t q_swz(uint32_t i) { return EZLDA_QSWZ ? (i ^ ((i >> 5) & 31u)) : i; }
+#ifndef EZLDA_WALK2
+#define EZLDA_WALK2 1
 #endif
 #ifndef EZLDA_SEGW_SMALL
 #define EZLDA_SEGW_SMALL 16u  // S' segment width when K <= kSegCap x 16 (16 or 32 entries per lane and round)
@@ -899,9 +909,23 @@ __device__ __forceinline__ unsigned long long entry_mac(uint32_t w, uint32_t row
   return acc + (unsigned long long)(w & 0xFFFFu) * lds_u32(row_s + off);
 }
 
+#ifndef EZLDA_MAC2
+#define EZLDA_MAC2 0
+#endif
 template <uint32_t kDTs>
 __device__ __forceinline__ unsigned long long sector_mac(unsigned long long acc, const uint4& a, const uint4& b,
                                                          uint32_t row_s) {
+#if EZLDA_MAC2  // two independent IMAD.WIDE chains (half the dependent latency per sector)
+  unsigned long long t = entry_mac<kDTs>(a.y, row_s, 0ull);
+  acc = entry_mac<kDTs>(a.x, row_s, acc);
+  t = entry_mac<kDTs>(a.w, row_s, t);
+  acc = entry_mac<kDTs>(a.z, row_s, acc);
+  t = entry_mac<kDTs>(b.y, row_s, t);
+  acc = entry_mac<kDTs>(b.x, row_s, acc);
+  t = entry_mac<kDTs>(b.w, row_s, t);
+  acc = entry_mac<kDTs>(b.z, row_s, acc);
+  return acc + t;
+#endif
   acc = entry_mac<kDTs>(a.x, row_s, acc);
   acc = entry_mac<kDTs>(a.y, row_s, acc);
   acc = entry_mac<kDTs>(a.z, row_s, acc);
@@ -954,9 +978,18 @@ __device__ __forceinline__ uint32_t packed_count(const uint32_t* E, uint32_t nnz
   }
   return 0u;
 }
-// D[d][k] of a packed D row / W[v][k] of a packed tail row
+// D[d][k] of a packed D row (logical index -> address by d_at) / W[v][k] of a packed tail row
 __device__ __forceinline__ uint32_t row_count(const Dev& d, const uint32_t* E, uint32_t nnz, uint32_t k) {
-  return packed_count(E, nnz, k, d.dt);
+  uint32_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((__ldg(E + d_at(d.dperm, mid)) >> d.dt) < k) lo = mid + 1u; else hi = mid;
+  }
+  if (lo < nnz) {
+    const uint32_t w = __ldg(E + d_at(d.dperm, lo));
+    if ((w >> d.dt) == k) return w & 0xFFFFu;
+  }
+  return 0u;
 }
 __device__ __forceinline__ uint32_t tail_count(const uint32_t* E, uint32_t nnz, uint32_t k) {
   return packed_count(E, nnz, k, 16u);
@@ -1016,7 +1049,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
   {
     WCursor wc = wcursor(d, cur, v);
     for (uint32_t e = 0; e < nnz; ++e) {
-      const uint32_t w = __ldg(E + e);
+      const uint32_t w = __ldg(E + d_at(d.dperm, e));
       const uint32_t k = d_topic(w, d.dt);
       if (kMerge) {
         const uint32_t c = wc.at(k);
@@ -1039,7 +1072,7 @@ __device__ uint32_t exact_draw(const Dev& d, const Buf& cur, uint32_t v, const W
     uint32_t last = K1;
     WCursor wc = wcursor(d, cur, v);
     for (uint32_t e = 0; e < nnz; ++e) {
-      const uint32_t w = __ldg(E + e);
+      const uint32_t w = __ldg(E + d_at(d.dperm, e));
       const uint32_t k = d_topic(w, d.dt);
       const uint32_t c = kMerge ? wc.at(k) : 0u;
       if (k == K1) continue;
@@ -1184,6 +1217,10 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
 #else
   constexpr bool kPf = false;
 #endif
+  // sector-interleaved D rows (kernels.h d_phys): the K <= 4096 kernel, 16-entry segments
+  // (runtime: create picks the layout per shard, dperm_of)
+  const bool kPerm = kDPermOn && kSub == 8u && d.dperm;
+  static_assert(!(kDPermOn && kSub == 8u) || (kSegW == 16u && kPf), "interleaved D rows assume 16-entry segments, prefetched");
   uint4 fa = make_uint4(0u, 0u, 0u, 0u), fb = fa, fc = fa, fd = fa;  // prefetched round (kPf)
   uint32_t f_soff = 0;
   auto round_load = [&](uint32_t B0, uint32_t& o_soff, uint4& qa, uint4& qb, uint4& qc, uint4& qd) {
@@ -1192,11 +1229,14 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     o_soff = __shfl_sync(kFull, soff, slot);
     const uint32_t s_ebase = __shfl_sync(kFull, ebase, slot);
     const uint32_t s_nnz = __shfl_sync(kFull, nnz, slot);
-    const uint32_t e0 = (g - o_soff) * 16u;
-    const uint32_t* p = d.D + s_ebase + e0;
+    const uint32_t sg = g - o_soff, e0 = sg * 16u;  // segment of the row, its first logical entry
+    // interleaved rows: the segment's two sectors are physical sectors g%4 and 4 + g%4 of its
+    // 64-entry block (consecutive lanes fill whole lines); else consecutive
+    const uint32_t* p = d.D + s_ebase + (kPerm ? ((sg >> 2) * 64u + (sg & 3u) * 8u) : e0);
+    const uint32_t kSec2 = kPerm ? 32u : 8u;
     qa = qb = qc = qd = make_uint4(0u, 0u, 0u, 0u);
     if (g < T && e0 < s_nnz) ldg256(p, qa, qb);
-    if (g < T && e0 + 8u < s_nnz) ldg256(p + 8u, qc, qd);
+    if (g < T && e0 + 8u < s_nnz) ldg256(p + kSec2, qc, qd);
   };
   if (kPf) round_load(0u, f_soff, fa, fb, fc, fd);
   for (uint32_t B0 = 0; B0 < T; B0 += 32u) {
@@ -1337,9 +1377,29 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
 #ifdef EZLDA_EXP_FAKEROW
           ldg256(g_fake + ((s_ebase + 16u * ((a - c0) >> 1)) & 0x3F0u) + 8u * ((a - c0) & 1u), qa, qb);
 #else
-          ldg256(E + (a - c0) * 8u, qa, qb);
+          ldg256(E + (kPerm ? d_phys((a - c0) * 8u) : (a - c0) * 8u), qa, qb);
 #endif
           const uint32_t wv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+#if EZLDA_WALK2
+          // the candidate is the first entry whose running prefix passes Yf.  No K1 or padding
+          // test is needed: m[K1] = 0 and padding (w = 0) add 0, and the prefix before the chunk
+          // (base) is <= Yf, so neither can be the first to pass.  Branch-free: pb = the last
+          // prefix <= Yf, wsel = the entry where the prefix crosses; pa = pb + its product.
+          {
+            unsigned long long q = pa;
+            uint32_t wsel = 0u;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const unsigned long long qn = entry_mac<kDTs>(wv[e], row_s, q);
+              const bool le = qn <= Yf;
+              if (le) pb = qn;
+              if (!le && q <= Yf) wsel = wv[e];
+              q = qn;
+            }
+            topic = d_topic(wsel, kDTs);
+            pa = entry_mac<kDTs>(wsel, row_s, pb);
+          }
+#else
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t w = wv[e];
@@ -1350,6 +1410,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
               pa = q;
             }
           }
+#endif
         } else {
           // walk the chunk two sectors (16 entries) at a time from registers: one memory
           // round trip per 16 entries instead of one per entry
@@ -1389,7 +1450,7 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
           // (HBM table: L1-cached loads, coherent within the SM -- a warp-staged item's table is
           // written inside this kernel by a warp of the same block, published by the slot's
           // release / acquire)
-          auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldca(qfx + i) : qfx[i]; };
+          auto qv = [&](uint32_t i) -> uint32_t { return kQG ? __ldca(qfx + q_swz(i)) : qfx[q_swz(i)]; };
           {  // first the 32-topic chunk from the contiguous chunk ends
             uint32_t ca = 0, cb = d.nch - 1u;
             while (ca < cb) {
@@ -1555,8 +1616,18 @@ __device__ void stage_row_warp(const Dev& d, const Buf& cur, uint32_t v, const W
       q4.y = __double2uint_rn(fmin(d.alpha * (base + p1) * two_t, 4294967295.0));
       q4.z = __double2uint_rn(fmin(d.alpha * (base + p2) * two_t, 4294967295.0));
       q4.w = __double2uint_rn(fmin(d.alpha * (base + p3) * two_t, 4294967295.0));
-      *reinterpret_cast<uint4*>(qfx + kb) = q4;
       if ((lane & 7u) == 7u) ce[(kb + 3u) >> 5] = q4.w;
+#if EZLDA_QSWZ
+      {  // swizzled store (q_swz): topic kb + t at (kb ^ (x & ~3)) + (t ^ (x & 3)), x = chunk & 31
+        const uint32_t x = (kb >> 5) & 31u;
+        uint32_t t;  // element p of the stored vector = topic kb + (p ^ (x & 3)): swap pairs, then halves
+        if (x & 1u) { t = q4.x; q4.x = q4.y; q4.y = t; t = q4.z; q4.z = q4.w; q4.w = t; }
+        if (x & 2u) { t = q4.x; q4.x = q4.z; q4.z = t; t = q4.y; q4.y = q4.w; q4.w = t; }
+        *reinterpret_cast<uint4*>(qfx + (kb ^ (x & ~3u))) = q4;
+      }
+#else
+      *reinterpret_cast<uint4*>(qfx + kb) = q4;
+#endif
     }
     carry = carry + __shfl_sync(kFull, incl, 31);
   }
@@ -2053,7 +2124,7 @@ __global__ void __launch_bounds__(kLlptWarps * 32) k_llpt(Dev d, Buf cur, double
       double S = 0.0;
       for (uint32_t e0 = 0; e0 < nnz; e0 += 8u) {
         uint4 qa, qb;
-        ldg256(Drow + e0, qa, qb);
+        ldg256(Drow + d_at(d.dperm, e0), qa, qb);
         const uint32_t ev[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i)  // padding entries are 0: count 0 adds +0
@@ -2128,7 +2199,7 @@ __global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) 
     const double* qp = d.tbq + (size_t)v * d.Kpad;
     double S = 0.0;
     for (uint32_t e = 0; e < nnz; ++e) {
-      const uint32_t w = __ldg(E + e);
+      const uint32_t w = __ldg(E + d_at(d.dperm, e));
       S = S + (double)(w & 0xFFFFu) * __ldg(wh + d_topic(w, d.dt));
     }
     const double Q = __ldg(qp + d.K - 1u);
@@ -2139,7 +2210,7 @@ __global__ void __launch_bounds__(256) k_tb_draw(Dev d, Buf nxt, uint32_t iter) 
       const double up = u * Z;
       double acc = 0.0;
       for (uint32_t e = 0; e < nnz; ++e) {
-        const uint32_t w = __ldg(E + e);
+        const uint32_t w = __ldg(E + d_at(d.dperm, e));
         const uint32_t k = d_topic(w, d.dt);
         acc = acc + (double)(w & 0xFFFFu) * __ldg(wh + k);
         topic = k;
@@ -2191,7 +2262,7 @@ __global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32
     const uint32_t* E = d.D + base + kDHdr;
     double S = 0.0;
     for (uint32_t e = 0; e < nnz; ++e) {
-      const uint32_t w = __ldg(E + e);
+      const uint32_t w = __ldg(E + d_at(d.dperm, e));
       S = S + (double)(w & 0xFFFFu) * wh[d_topic(w, d.dt)];
     }
     const double Z = S + Q;
@@ -2203,7 +2274,7 @@ __global__ void __launch_bounds__(256) k_tb_item(Dev d, Buf cur, Buf nxt, uint32
         const double up = u * Z;
         double acc = 0.0;
         for (uint32_t e = 0; e < nnz; ++e) {
-          const uint32_t w = __ldg(E + e);
+          const uint32_t w = __ldg(E + d_at(d.dperm, e));
           const uint32_t k = d_topic(w, d.dt);
           acc = acc + (double)(w & 0xFFFFu) * wh[k];
           topic = k;
@@ -2265,6 +2336,7 @@ size_t llpt_smem_bytes(uint32_t K) {  // row | T | CP
 // segment (K > 4096: the descent walks two sectors from registers); runs longer than kSegCap x
 // 16 nonzeros (large K only) take a fallback with fb-entry segments, fb a power of two with
 // K <= kSegCap x fb.
+static_assert(kDPermMaxK == kSegCap * 16u, "interleaved D rows iff the <16, 8> sampler kernel (K <= kSegCap x 16)");
 void seg_config(uint32_t K, uint32_t* segw, uint32_t* sub, uint32_t* fb) {
   *segw = 16u;
   if (K <= kSegCap * 16u) {

@@ -41,6 +41,24 @@ __host__ __device__ __forceinline__ uint32_t d_shift(uint32_t K) { return K <= k
 __host__ __device__ __forceinline__ uint32_t d_entry(uint32_t k, uint32_t c, uint32_t dt) { return (k << dt) | c; }
 __host__ __device__ __forceinline__ uint32_t d_topic(uint32_t w, uint32_t dt) { return w >> dt; }
 constexpr uint32_t kDHdr = 8;  // header words in front of every packed D row (one 32 B sector)
+// Sector-interleaved D rows (K <= 4096, Dev::dperm).  The sampler reads a row as 16-entry
+// segments, one per lane, two 32-byte sectors each; stored in topic order, the first load of a
+// warp (sector 0 of 32 consecutive segments) would touch 16 lines and use half of each.  So the
+// entries are kept in 64-entry blocks (two 128-byte lines, the row's entries starting on a line)
+// whose logical (topic-sorted) sector s = 2 g + h of the block's segment g is stored at physical
+// sector 4 h + g: the first sectors of a block's four segments fill one line, the second
+// sectors the other.  Logical order (and every prefix, checkpoint and search) is unchanged;
+// only addresses are mapped.
+__host__ __device__ __forceinline__ uint32_t d_psec(uint32_t s) { return ((s & 1u) << 2) | ((s >> 1) & 3u); }
+__host__ __device__ __forceinline__ uint32_t d_phys(uint32_t e) {  // logical entry -> physical word
+  return (e & ~63u) | (d_psec((e >> 3) & 7u) << 3) | (e & 7u);
+}
+__host__ __device__ __forceinline__ uint32_t d_at(uint32_t perm, uint32_t e) { return perm ? d_phys(e) : e; }
+#ifndef EZLDA_DPERM
+#define EZLDA_DPERM 1
+#endif
+constexpr bool kDPermOn = EZLDA_DPERM != 0;  // build switch (A/B): 0 keeps every row in topic order
+constexpr uint32_t kDPermMaxK = 4096;  // the interleaved layout is used iff K <= this (sampler <16, 8> path)
 #ifndef EZLDA_SEGCAP
 #define EZLDA_SEGCAP 256
 #endif
@@ -75,13 +93,14 @@ struct Dev {
   uint32_t segsub;  // entries per S' checkpoint chunk (8: one per sector; or segw)
   uint32_t segfb;   // fallback segment width for runs longer than kSegCap x segw (0: none)
   uint32_t dt;      // topic shift of the packed D entries (d_shift(K))
+  uint32_t dperm;   // 1: sector-interleaved D rows (d_phys; K <= kDPermMaxK), entries 128-byte aligned
   uint32_t grp;     // runs per sampler work claim (32; smaller at large K, sampler_group_runs)
   double alpha, beta, Vbeta;
   uint64_t seed, token_base;
   PhiloxKeys pk;   // Philox round keys of seed (philox_keys)
   // static structure
   const uint32_t* dofs;
-  const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 8 words)
+  const uint32_t* ddb;     // [Dn] D-row base of each doc (multiple of 8 words; dperm: 24 mod 32)
   const uint32_t* tw;
   const uint2* twr;       // [N] (tw, run id) per doc-major token (doc pass: one 8-byte load)
   const uint32_t* run_j0;

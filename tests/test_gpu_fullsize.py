@@ -1,4 +1,4 @@
-"""Parity at the benchmarked size: the PubMed-shaped corpus (8.2 M docs, V = 141,043,
+"""Parity at the benchmarked sizes: the PubMed-shaped corpus (8.2 M docs, V = 141,043,
 738 M tokens, K = 1000) in the launch configuration bench.py times (default options: hybrid
 W, 10,000-token regions, 32 MiB doc windows -- about 94 windows, so hot-word items are cut
 at window boundaries and the 3-slot pipeline runs over ~200k items).
@@ -28,13 +28,16 @@ def _w_counts(w, z, V, K, chunk=1 << 26):
     return W.reshape(V, K).astype(np.int32)
 
 
-def test_pubmed_full_size_sampled_parity(oracle_mod):
+@pytest.mark.parametrize("config,n_sample_docs", [("pubmed", 1300), ("nytimes", 400)])
+def test_full_size_sampled_parity(oracle_mod, config, n_sample_docs):
+    """PubMed-shaped (short docs: topic-ordered D rows) and NYTimes-shaped (99.5 M tokens,
+    332 tokens per doc: the sector-interleaved D rows, kernels.h d_phys) at full size."""
     import torch
 
     from paper_2007_08725_b200 import lda
     from paper_2007_08725_b200.synth import planted_corpus_torch
 
-    cfg = CONFIGS["pubmed"]
+    cfg = CONFIGS[config]
     K, V = cfg.K, cfg.V
     w_t, d_t = planted_corpus_torch(cfg.n_docs, cfg.V, cfg.mean_len, cfg.sigma, cfg.K_true, cfg.zipf_s,
                                     seed=CORPUS_SEED, device="cuda")
@@ -44,13 +47,13 @@ def test_pubmed_full_size_sampled_parity(oracle_mod):
     del w_t, d_t
     torch.cuda.empty_cache()
     N = len(w)
-    assert N > 7e8
+    assert N > (7e8 if config == "pubmed" else 9e7)
     L = np.bincount(d, minlength=cfg.n_docs)
     dofs = np.concatenate([[0], np.cumsum(L)])
     assert np.all(np.diff(d.astype(np.int64)) >= 0), "recipe emits doc-grouped tokens"
 
     rng = np.random.default_rng(2024)
-    docs = np.sort(rng.choice(cfg.n_docs, size=1300, replace=False))
+    docs = np.sort(rng.choice(cfg.n_docs, size=n_sample_docs, replace=False))
     top = int(np.argmax(np.bincount(w, minlength=V)))
     top_pos = np.nonzero(w == top)[0]
     top_pick = np.sort(rng.choice(top_pos, size=2000, replace=False))
@@ -111,5 +114,5 @@ def test_pubmed_full_size_sampled_parity(oracle_mod):
             row[col[rp[v]:rp[v + 1]].astype(np.int64)] = val[rp[v]:rp[v + 1]]
             assert np.array_equal(row, Wn[v]), (it, v)
         del Wc, Wn
-    print(f"full-size PubMed-shaped: {checked} sampled draws over 2 iterations, 0 mismatches")
+    print(f"full-size {config}-shaped: {checked} sampled draws over 2 iterations, 0 mismatches")
     assert checked >= 2 * 100_000

@@ -458,6 +458,13 @@ DEBUG_CASES = {
     "c1_lookup_K64": (SMALL, 64, 3, 2),
     "c1_lookup_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 2, 2),
     "both_K5000": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 5000, 2, 3),
+    # sector-interleaved D rows (kernels.h d_phys) forced on short docs / off on long docs, and
+    # with the C1 lookup (binary search through the mapped row)
+    "dperm_on_K64": (SMALL, 64, 3, 4),
+    "dperm_on_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 3, 4),
+    "dperm_on_c1_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 2, 6),
+    "dperm_on_K4096": (dict(n_docs=100, V=2000, mean_len=300.0, sigma=0.8, K_true=50, seed=21), 4096, 2, 4),
+    "dperm_off_K1000": (dict(n_docs=60, V=3000, mean_len=1200.0, sigma=0.6, K_true=100, seed=5), 1000, 2, 8),
 }
 
 
@@ -467,8 +474,11 @@ def test_rare_paths_parity(ez, oracle_mod, case):
     one-step parity with the oracle, bit-identical topics and exact counts."""
     spec, K, iters, flags = DEBUG_CASES[case]
     w, d = planted_corpus_np(**spec)
-    run_one_step_parity(ez, oracle_mod, w, d, spec["n_docs"], spec["V"], K, iters, check_every=iters,
-                        debug_flags=flags)
+    gpu, orc = run_one_step_parity(ez, oracle_mod, w, d, spec["n_docs"], spec["V"], K, iters, check_every=iters,
+                                   debug_flags=flags)
+    # LLPT reads every packed D row (through the interleaved layout when dperm is on)
+    lg, lo = gpu.loglik(), orc.loglik(1)
+    assert abs(lg - lo) <= 1e-10 * abs(lo), (lg, lo)
 
 
 def test_live_handles_with_different_K(ez, oracle_mod, tiny):

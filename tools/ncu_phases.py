@@ -44,12 +44,18 @@ def region_of(regs, ln):
     return r
 
 
+OUTER = {"arm_slot", "item_epilogue_warp", "stage_row_warp", "exact_draw", "mpt_token", "doc_tokens_skip_test",
+         "flag_run", "item_epilogue"}
+
+
 def main(rep, src_dir):
     regs = {fn: regions(os.path.join(src_dir, fn)) for fn in ("kernels.cu", "device.cuh")}
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     cur_file, hdr, line_no = None, None, None
-    agg = collections.defaultdict(lambda: [0.0, 0.0])
+    # an inlined SASS instruction is listed under every source line of its inline chain: keep one
+    # attribution per address, preferring the outermost region (a phase, a kernel) over a helper
+    occ = collections.defaultdict(list)
     for row in csv.reader(io.StringIO(out)):
         if not row:
             continue
@@ -65,14 +71,23 @@ def main(rep, src_dir):
             continue
         if row[0].strip():
             line_no = int(row[0])
-        if len(row) > 4 and row[2].strip():
+        if len(row) > 7 and row[2].strip() and row[2] != "..." and row[2] != "-":
             try:
                 st, ex = float(row[4] or 0), float(row[7] or 0)
             except ValueError:
                 continue
-            key = f"{cur_file}:{region_of(regs[cur_file], line_no)}" if cur_file in regs else cur_file
-            agg[key][0] += st
-            agg[key][1] += ex
+            reg = region_of(regs[cur_file], line_no) if cur_file in regs else ""
+            occ[row[2]].append((cur_file, reg, st, ex))
+    agg = collections.defaultdict(lambda: [0.0, 0.0])
+    for addr, lst in occ.items():
+        def pri(o):
+            f, reg, _, _ = o
+            if f == "kernels.cu" and (reg.startswith("sample_batch") or reg.startswith("k_") or reg in OUTER):
+                return 0
+            return 1 if f == "kernels.cu" else 2
+        f, reg, st, ex = sorted(lst, key=pri)[0]
+        agg[f"{f}:{reg}" if reg else f][0] += st
+        agg[f"{f}:{reg}" if reg else f][1] += ex
     tst = sum(v[0] for v in agg.values()) or 1.0
     tex = sum(v[1] for v in agg.values()) or 1.0
     print(f"executed warp-instructions (source attribution) {tex:.4g}")
