@@ -143,11 +143,14 @@ __device__ __forceinline__ double mpt_den(const WordRec& r, double M, uint32_t C
 // The MPT decision u < thr with thr = M / den rounded as the oracle rounds it.  The
 // division is skipped when u den is clear of M by a relative 2^-50 (then u < M / den
 // and u < fl(M / den) agree); otherwise thr is formed exactly as written.
+// (the division sits in a call of its own: inlined, the compiler speculates it -- MUFU.RCP64H
+// and eight DFMA per token -- ahead of the two comparisons that almost always decide)
+static __device__ __noinline__ bool mpt_skip_exact(double u, double M, double den) { return u < M / den; }
 __device__ __forceinline__ bool mpt_skip(double u, double M, double den) {
   const double p = u * den;
   if (p < M * (1.0 - 0x1p-50)) return true;
   if (p > M * (1.0 + 0x1p-50)) return false;
-  return u < M / den;
+  return mpt_skip_exact(u, M, den);
 }
 
 }  // namespace ezl

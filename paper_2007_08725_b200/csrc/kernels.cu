@@ -467,9 +467,9 @@ __device__ __forceinline__ uint32_t row_lookup(const uint16_t* keys, const uint1
 // the sampler's marker) and returns true if the token failed the test (its run must be flagged).
 template <typename LookupF>
 __device__ __forceinline__ bool mpt_token(const Dev& d, const Buf& nxt, uint32_t j, uint32_t L, uint32_t iter,
-                                          uint32_t v, LookupF C, unsigned long long& n_skip) {
+                                          uint32_t v, LookupF C, unsigned long long& n_skip, bool g2) {
   WordRec r;
-  if (d.geff <= 2) {  // compact view: one 32-byte load + one 4-byte load
+  if (g2) {  // g <= 2 (a warp-uniform kernel argument): compact view, one 32-byte load + one 4-byte load
     const WordRecM m = d.recm[v];
     const uint32_t kk = __ldg(d.reck + v);
     r.a[0] = m.a0;
@@ -550,7 +550,7 @@ __device__ __forceinline__ void doc_tokens_skip_test(const Dev& d, const Buf& nx
 __host__ __device__ __forceinline__ uint32_t doc_hist_stride(uint32_t Kpad) {
   return (Kpad / 2u + Kpad / 32u + 3u) & ~3u;
 }
-template <bool kSkipTest>
+template <bool kSkipTest, bool kG2 = true>  // kG2: S_est depth g <= 2 (the compact record view)
 #ifndef EZLDA_DOC_PF
 #define EZLDA_DOC_PF 1
 #endif
@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       for (uint32_t c = 0; c < kPre; ++c) {
         if (32u * c >= L) break;  // warp-uniform
         bool f = false;
-        if (lane + 32u * c < L) f = mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], C, n_skip);
+        if (lane + 32u * c < L) f = mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], C, n_skip, kG2);
 #ifndef EZLDA_EXP_DOC_NOFLAG  // diagnostic: no flag atomics (the sampler then sees no flagged run)
         flag_run(d, f, pr[c]);
 #endif
@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
         if (i < L) {
           const uint2 wr = d.twr[j0 + i];
           rid = wr.y;
-          f = mpt_token(d, nxt, j0 + i, L, iter, wr.x, C, n_skip);
+          f = mpt_token(d, nxt, j0 + i, L, iter, wr.x, C, n_skip, kG2);
         }
         flag_run(d, f, rid);
       }
@@ -2471,6 +2471,7 @@ cudaError_t configure_kernels(uint32_t K, uint32_t* grid) {
     const int dh = kDocWarps * (int)doc_hist_stride((K + 31) / 32 * 32) * 4;
     if ((e = raise_smem(dev, (const void*)k_doc_hist<false>, dh))) return e;
     if ((e = raise_smem(dev, (const void*)k_doc_hist<true>, dh))) return e;
+    if ((e = raise_smem(dev, (const void*)k_doc_hist<true, false>, dh))) return e;
   }
   return cudaSuccess;
 }
@@ -2507,8 +2508,10 @@ void launch_doc_pass(const Dev& d, const Buf& cur, const Buf& nxt, const uint32_
   if (n_w && d.K <= 4096) {
     const uint32_t grid = std::min<uint32_t>((n_w + kDocWarps - 1) / kDocWarps, 148u * 16u);
     const size_t smem = (size_t)kDocWarps * doc_hist_stride(d.Kpad) * 4;
-    if (skip_test)
+    if (skip_test && d.geff <= 2)
       k_doc_hist<true><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
+    else if (skip_test)
+      k_doc_hist<true, false><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
     else
       k_doc_hist<false><<<grid, kDocWarps * 32, smem, s>>>(d, cur, nxt, docs_w, n_w, iteration);
   } else if (n_w) {
