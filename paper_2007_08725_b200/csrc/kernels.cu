@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       if (b) bmp[wi] = 0u;
       nnz += __shfl_sync(kFull, incl, 31);
     }
-    for (uint32_t p = nnz + lane; p < ((nnz + 7u) & ~7u); p += 32) Drow[d_at(d.dperm, p)] = 0u;  // pad to 8
+    if (nnz + lane < ((nnz + 7u) & ~7u)) Drow[d_at(d.dperm, nnz + lane)] = 0u;  // pad to 8 (< 8 entries)
     if (lane == 0) {
       Drow[-(int)kDHdr] = (L << 16) | nnz;
       Drow[1 - (int)kDHdr] = j0;
@@ -843,6 +843,12 @@ __device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over
 // i ^ (chunk & 31)): the lanes of a warp search different chunks in step, so an unswizzled
 // table sends them all to the same bank (e.g. every lane's first probe is entry 15 of its chunk)
 __device__ __forceinline__ uint32_t q_swz(uint32_t i) { return EZLDA_QSWZ ? (i ^ ((i >> 5) & 31u)) : i; }
+#ifndef EZLDA_RED_SHARED
+#define EZLDA_RED_SHARED 1
+#endif
+#ifndef EZLDA_HDR_PF
+#define EZLDA_HDR_PF 0
+#endif
 #ifndef EZLDA_WALK2
 #define EZLDA_WALK2 1
 #endif
@@ -1168,6 +1174,12 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
   constexpr uint32_t kCap = (kSub == 8u ? 2u * kSegCap : kSegCap) / kCk;  // segments per batch
   const uint32_t nb = __popc(__ballot_sync(kFull, lane < nc && sincl <= kCap));
   if (nb == 0) return 0;  // the first run alone exceeds a batch: the caller takes its wide-segment path
+#if EZLDA_HDR_PF
+  // the D-row bases of the runs already queued for the next batch, loaded now; their header
+  // lines are prefetched into L2 once phase B is done (the next phase A then hits L2)
+  uint32_t pf_dbase = 0xFFFFFFFFu;
+  if (nb + lane < qn) pf_dbase = __ldg(d.run_dbase + lds_u32v(ws_q_at(ws, nb + lane)));
+#endif
   const uint32_t T = __shfl_sync(kFull, sincl, nb - 1u);
   const uint32_t soff = sincl - nseg;
 #if EZLDA_SCAN_DYN
@@ -1311,6 +1323,9 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     carry = __shfl_sync(kFull, acc, 31);
   }
   __syncwarp();
+#if EZLDA_HDR_PF
+  if (pf_dbase != 0xFFFFFFFFu) asm volatile("prefetch.global.L2 [%0];" ::"l"(d.D + pf_dbase));
+#endif
   // ---- D: lane per token.  The doc pass left a marker in z^i for the tokens that failed
   //      the MPT test (the others already hold K1): 0x8000 | min(C1, 0x7FFF) when K <=
   //      32768 (d.zmark), else 0xFFFF.
@@ -1481,6 +1496,8 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (d.hist_bitmap) {
       if (atomicAdd(&hist[topic], 1u) == 0u)  // first token of this topic in the item: mark it
         atomicOr(&hist[d.Kpad + (topic >> 5)], 1u << (topic & 31u));
+    } else if (EZLDA_RED_SHARED && !d.hist_global) {  // shared-space reduction (not a generic atomic)
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(hist + topic)) : "memory");
     } else {
       atomicAdd(&hist[topic], 1u);
     }
