@@ -843,6 +843,12 @@ __device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over
 // i ^ (chunk & 31)): the lanes of a warp search different chunks in step, so an unswizzled
 // table sends them all to the same bank (e.g. every lane's first probe is entry 15 of its chunk)
 __device__ __forceinline__ uint32_t q_swz(uint32_t i) { return EZLDA_QSWZ ? (i ^ ((i >> 5) & 31u)) : i; }
+#ifndef EZLDA_LARGEK_1BLK
+#define EZLDA_LARGEK_1BLK 0  // A/B: 1 block x 3-4 slots at K = 10k 42.5 -> 57-59 ms (profiles/r02/ab_dperm.log)
+#endif
+#ifndef EZLDA_SPIN_MAX
+#define EZLDA_SPIN_MAX 256  // longest nanosleep (ns) of the sampler's slot wait
+#endif
 #ifndef EZLDA_RED_SHARED
 #define EZLDA_RED_SHARED 1
 #endif
@@ -1883,7 +1889,15 @@ __global__ void __launch_bounds__(kSampWarpsP * 32, EZLDA_SAMP_MINB) k_sampler(D
     SlotCtl& c = ctl[sl];
     uint32_t st = 0;
     if (lane == 0) {
+#if EZLDA_SPIN_MAX > 32
+      uint32_t ns = 32u;  // exponential backoff: fewer spin instructions competing for issue
+      while (((st = ld_acquire_s(&c.state)) & ~kExit) != k) {
+        __nanosleep(ns);
+        ns = min(2u * ns, (uint32_t)EZLDA_SPIN_MAX);
+      }
+#else
       while (((st = ld_acquire_s(&c.state)) & ~kExit) != k) __nanosleep(32);
+#endif
     }
     st = __shfl_sync(kFull, st, 0);
     __syncwarp();  // orders lane 0's acquire before the other lanes' reads of the slot
@@ -2389,7 +2403,10 @@ SamplerLayout sampler_layout(uint32_t K) {
   // table in shared memory, else the histograms in HBM scratch, else also the Q' table in
   // HBM; last resort one block per SM
   const size_t budgets[2] = {(228u * 1024u) / EZLDA_SAMP_MINB - 1024u, kMaxSmem};
-  for (size_t budget : budgets)
+  for (size_t budget : budgets) {
+    // large K (EZLDA_LARGEK_1BLK): one block per SM with more slots rather than two blocks with
+    // two -- a block's warps can run at most nslots - 1 items ahead of its slowest warp
+    if (EZLDA_LARGEK_1BLK && K > kSegCap * 16u && budget != kMaxSmem) continue;
     for (uint32_t n = kMaxSlots; n >= 1; --n) {
       if (n < 2u && budget != kMaxSmem) break;  // keep >= 2 slots when blocks share the SM
       for (uint32_t mode = 0; mode < 3; ++mode) {
@@ -2406,6 +2423,7 @@ SamplerLayout sampler_layout(uint32_t K) {
         }
       }
     }
+  }
   return L;
 }
 uint32_t sampler_slots(uint32_t K) { return sampler_layout(K).nslots; }
