@@ -1053,6 +1053,7 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
   EZ_ALLOC(h, d.inv_den, double, h->K);
   if (h->K > 4096u && h->Vt && h->branches == 3) {  // absent-pair order of the tail records
     EZ_ALLOC(h, d.w0ord, uint32_t, h->K);
+    EZ_ALLOC(h, d.twv, double, std::max<uint64_t>(h->tail_cap, 1));  // What of the tail nonzeros
     EZ_ALLOC(h, h->w0_key_in, unsigned long long, h->K);
     EZ_ALLOC(h, h->w0_key_out, unsigned long long, h->K);
     EZ_ALLOC(h, h->w0_top_in, uint32_t, h->K);

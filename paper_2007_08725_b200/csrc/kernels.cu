@@ -399,11 +399,27 @@ __global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
   Top4 tp;
   top4_init(tp);
   WordRec r;
+  double* tv = act ? d.twv + d.tofs[t] : nullptr;  // the nonzeros' What, for the lockstep pass
   if (act) {
-    for (uint32_t e = 0; e < n; ++e) {
-      const uint32_t p = tr[e];
-      const uint32_t k = p >> 16;
-      top4_insert(tp, ((double)(p & 0xFFFFu) + d.beta) / d.den[k], k);
+    // 16 entries per step with their loads and den gathers issued together: the heaviest tail
+    // words (thousands of nonzeros) set the kernel's time, and one dependent load pair per
+    // entry left them latency-bound
+    constexpr uint32_t kU = 16;
+    for (uint32_t e0 = 0; e0 < n; e0 += kU) {
+      uint32_t pp[kU];
+      double dd[kU];
+#pragma unroll
+      for (uint32_t i = 0; i < kU; ++i) pp[i] = (e0 + i < n) ? __ldg(tr + e0 + i) : 0u;
+#pragma unroll
+      for (uint32_t i = 0; i < kU; ++i) dd[i] = (e0 + i < n) ? __ldg(d.den + (pp[i] >> 16)) : 1.0;
+#pragma unroll
+      for (uint32_t i = 0; i < kU; ++i) {
+        if (e0 + i < n) {
+          const double w = ((double)(pp[i] & 0xFFFFu) + d.beta) / dd[i];
+          tv[e0 + i] = w;
+          top4_insert(tp, w, pp[i] >> 16);
+        }
+      }
     }
     uint32_t found = 0;
     for (uint32_t i = 0; found < 4u && i < d.K; ++i) {
@@ -423,7 +439,11 @@ __global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
   const uint32_t K1 = r.K[0];
   double* qe = d.qexact + (size_t)(act ? v : 0u) * d.nch;
   double acc = 0.0;
+  // the nonzeros' values were computed above (independent divisions); the lockstep chain only
+  // selects them, with the next nonzero's topic and value loaded one nonzero ahead (a division
+  // inside the divergent branch sat on every word's dependent chain: K = 10k 6 -> <1 ms)
   uint32_t e = 0, nk = n ? (tr[0] >> 16) : 0xFFFFFFFFu;
+  double nv = n ? tv[0] : 0.0;
   for (uint32_t c0 = 0; c0 < d.Kpad; c0 += kTailChunk) {  // (every thread of the block: barriers)
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < kTailChunk; i += blockDim.x)
@@ -433,9 +453,10 @@ __global__ void __launch_bounds__(128) k_word_rec_tail(Dev d, Buf cur) {
     for (uint32_t k = c0; k < cend; ++k) {
       double w = s_w0[k - c0];
       if (k == nk) {
-        w = ((double)(tr[e] & 0xFFFFu) + d.beta) / d.den[k];
+        w = nv;
         ++e;
         nk = (e < n) ? (tr[e] >> 16) : 0xFFFFFFFFu;
+        nv = (e < n) ? tv[e] : 0.0;
       }
       if (k == K1) w = 0.0;  // What' (Eq 6): adds +0, as the oracle skips K1
       acc = acc + w;

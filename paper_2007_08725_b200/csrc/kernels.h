@@ -126,6 +126,7 @@ struct Dev {
   double* den;    // [K] n_k + V beta
   double* what0;  // [K] beta / den_k (What of an absent (v, k) pair)
   uint32_t* w0ord;  // [K] topics by what0 desc, ties by topic asc (K > 4096 with tail words; per iteration)
+  double* twv;      // [tail capacity] What = (W + beta) / den_k of each tail nonzero (k_word_rec_tail scratch)
   double* inv_den;  // [K] 1 / den_k (the sampler's fixed-point heads, stage_row_warp)
   double* qexact;   // [V * nch] exact running sums P_v(32 c + 31) of the word-prep (exact redraws)
   unsigned char* wrow;  // [Vw * rs_bytes] sampler heads m | scales | qfx | ce (k_word_heads)
