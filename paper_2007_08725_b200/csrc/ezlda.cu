@@ -44,6 +44,8 @@ struct NcclApi {
   decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclCommDestroy) CommDestroy = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
 };
 
 NcclApi& nccl() {
@@ -61,8 +63,10 @@ NcclApi& nccl() {
       api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
       api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+      api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
       api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy &&
-               api.GetErrorString;
+               api.GetErrorString && api.GroupStart && api.GroupEnd;
     }
   }
   return api;
@@ -546,18 +550,33 @@ __global__ void k_tail_run_tok(const uint32_t* tokpre, uint32_t rt0, uint32_t R,
   if (r < R) out[r - rt0] = tokpre[r] - tokpre[rt0];
 }
 
-// W tail (world > 1): every rank's word-major tail topics -> the global packed tail rows
-ezlda_status merge_tail(ezlda* h, Buf& b) {
-  if (!h->multi || h->Vt == 0) return EZLDA_OK;
-  if (h->R > h->rt0) {
+// H7 (world > 1): the W merge.  The tail tokens' topics are gathered word-major
+// (k_tail_gather); the int32 all-reduce of the dense block and the u16 all-gather of the tail
+// topics are issued as ONE NCCL group, so the two collectives run concurrently; then every
+// rank rebuilds the global packed tail rows (integer sums: W is identical on every rank).
+ezlda_status exchange_w(ezlda* h, Buf& b) {
+  if (!h->multi) return EZLDA_OK;
+  const bool tail = h->Vt != 0;
+  if (tail && h->R > h->rt0) {
     k_tail_gather<<<(unsigned)((h->R - h->rt0 + 255) / 256), 256, 0, h->stream>>>(
         h->dev.run_j0, h->dev.run_len, h->tail_run_tok, h->rt0, h->R, b.z, h->tz_local);
     EZ_CUDA(h, cudaGetLastError());
   }
-  ezlda_status st = allgather(h, h->tz_local, h->tz_all, 2ull * h->tail_max);
-  if (st) return st;
-  ezl::launch_tail_rebuild(h->dev, b, h->tz_all, h->tail_off, (uint32_t)h->world, h->tail_max, h->stream);
-  EZ_CUDA(h, cudaGetLastError());
+  const size_t dense = (size_t)h->Vd * h->K, tbytes = tail ? 2ull * h->tail_max : 0;
+  ezlda_status st;
+  if (h->lgroup) {  // in-process test hook: the same sums / concatenation, one after the other
+    if ((st = allreduce(h, b.Wd, dense, ncclInt32))) return st;
+    if (tail && (st = allgather(h, h->tz_local, h->tz_all, tbytes))) return st;
+  } else {
+    EZ_NCCL(h, nccl().GroupStart());
+    if (dense) EZ_NCCL(h, nccl().AllReduce(b.Wd, b.Wd, dense, ncclInt32, ncclSum, h->comm, h->stream));
+    if (tbytes) EZ_NCCL(h, nccl().AllGather(h->tz_local, h->tz_all, tbytes, ncclUint8, h->comm, h->stream));
+    EZ_NCCL(h, nccl().GroupEnd());
+  }
+  if (tail) {
+    ezl::launch_tail_rebuild(h->dev, b, h->tz_all, h->tail_off, (uint32_t)h->world, h->tail_max, h->stream);
+    EZ_CUDA(h, cudaGetLastError());
+  }
   return EZLDA_OK;
 }
 
@@ -605,8 +624,7 @@ ezlda_status rebuild_counts(ezlda* h) {
   ezl::launch_sampler(h->dev, b, b, h->n_items, 0, true, h->stream);
   EZ_CUDA(h, cudaGetLastError());
   ezlda_status s;
-  if ((s = allreduce(h, b.Wd, (size_t)h->Vd * h->K, ncclInt32))) return s;
-  if ((s = merge_tail(h, b))) return s;
+  if ((s = exchange_w(h, b))) return s;
   ezl::launch_nk(h->dev, b, h->stream);  // n_k of the global W (identical on every rank)
   EZ_CUDA(h, cudaGetLastError());
   h->D_fresh = false;
@@ -1339,10 +1357,9 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     }
     EZ_CUDA(h, cudaGetLastError());
     ezlda_status st;
-    // H7 (world > 1): int32 all-reduce of the dense block and n_k, all-gather of
-    // the tail topics + tail-row rebuild (integer sums: W is identical on every rank)
-    if ((st = allreduce(h, nxt.Wd, (size_t)h->Vd * h->K, ncclInt32))) return st;
-    if ((st = merge_tail(h, nxt))) return st;
+    // H7 (world > 1): all-reduce of the dense block + all-gather of the tail
+    // topics (one NCCL group) + tail-row rebuild; n_k from the merged W
+    if ((st = exchange_w(h, nxt))) return st;
     if (h->multi) ezl::launch_nk(h->dev, nxt, s);  // n_k of the global W (identical on every rank)
     EZ_CUDA(h, cudaGetLastError());
     EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));
