@@ -112,8 +112,16 @@ typedef struct {
  * shards take when the rows do not fit).  C1_LOOKUP: the doc pass never carries C1 in the
  * z^i marker, so every sampled token looks C1 up in the packed D row (the path of
  * C1 >= 0x7FFF).  DPERM_ON / DPERM_OFF: force the sector-interleaved D-row layout on / off
- * (by default it is used when K <= 4096 and the shard averages >= 192 tokens per doc). */
-enum { EZLDA_DEBUG_NO_TAIL_ROWS = 1u, EZLDA_DEBUG_C1_LOOKUP = 2u, EZLDA_DEBUG_DPERM_ON = 4u, EZLDA_DEBUG_DPERM_OFF = 8u };
+ * (by default it is used when K <= 4096 and the shard averages >= 192 tokens per doc).
+ * NO_W_DELTA (world > 1): the dense W block is always exchanged as int32 local counts (by
+ * default it goes as packed 16-bit deltas against the previous W whenever they fit). */
+enum {
+  EZLDA_DEBUG_NO_TAIL_ROWS = 1u,
+  EZLDA_DEBUG_C1_LOOKUP = 2u,
+  EZLDA_DEBUG_DPERM_ON = 4u,
+  EZLDA_DEBUG_DPERM_OFF = 8u,
+  EZLDA_DEBUG_NO_W_DELTA = 16u
+};
 
 /* Compressed sparse rows of a count matrix, caller-allocated.  Pass col = val = NULL
  * to query nnz (row_ptr may also be NULL then).  row_ptr has rows+1 entries. */

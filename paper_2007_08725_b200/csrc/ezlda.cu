@@ -293,7 +293,14 @@ struct ezlda {
   uint16_t* tz_all = nullptr;       // [world * tail_max] gathered
   uint32_t* tail_run_tok = nullptr; // [R - rt0] word-major offset of a tail run's tokens in tz_local
   uint32_t* tail_off = nullptr;     // [world * (Vt + 1)] per-rank prefix of local tail counts
-  double exchange_bytes = 0;        // collective payload per iteration
+  double exchange_bytes = 0;        // collective payload of the last exchange
+  // dense-block deltas (world > 1): this rank's local counts of the last exchange, the packed
+  // 16-bit deltas, and a device flag "some |delta| does not fit"
+  int32_t* wloc_prev = nullptr;     // [Vd * K]
+  uint32_t* wpack = nullptr;        // [ceil(Vd * K / 2)]
+  int32_t* wover = nullptr;         // [1]
+  bool wloc_valid = false;          // wloc_prev holds the local counts of the previous exchange
+  uint64_t delta_exchanges = 0;     // exchanges that took the packed path (diagnostics)
   uint32_t* docs_w = nullptr;
   uint32_t* docs_b = nullptr;
   uint32_t* perm = nullptr;
@@ -473,7 +480,7 @@ bool group_barrier(LocalGroup* g) {
 
 ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t dt) {
   LocalGroup* g = static_cast<LocalGroup*>(h->lgroup);
-  const size_t esz = (dt == ncclInt32) ? 4 : 8;
+  const size_t esz = (dt == ncclInt32 || dt == ncclUint32) ? 4 : 8;
   EZ_CUDA(h, cudaStreamSynchronize(h->stream));
   {
     std::lock_guard<std::mutex> lk(g->m);
@@ -488,6 +495,9 @@ ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t d
   if (dt == ncclInt32)
     k_sum_ranks<int32_t><<<nb, 256, 0, h->stream>>>(reinterpret_cast<const int32_t* const*>(d_src), g->world, count,
                                                      static_cast<int32_t*>(tmp));
+  else if (dt == ncclUint32)
+    k_sum_ranks<uint32_t><<<nb, 256, 0, h->stream>>>(reinterpret_cast<const uint32_t* const*>(d_src), g->world, count,
+                                                      static_cast<uint32_t*>(tmp));
   else if (dt == ncclUint64)
     k_sum_ranks<unsigned long long><<<nb, 256, 0, h->stream>>>(
         reinterpret_cast<const unsigned long long* const*>(d_src), g->world, count,
@@ -550,29 +560,91 @@ __global__ void k_tail_run_tok(const uint32_t* tokpre, uint32_t rt0, uint32_t R,
   if (r < R) out[r - rt0] = tokpre[r] - tokpre[rt0];
 }
 
+// Dense-block deltas (SURVEY 8(e) "int16 deltas with an overflow guard").  delta = local -
+// prev (this rank's local counts now vs at the last exchange), packed two per u32 as 16-bit
+// fields delta + b, b = 32768 / world: every term lies in [1, 2b - 1] when |delta| < b, so the
+// u32 sum over the ranks of each field stays below 2^16 and never carries into its neighbour.
+// prev <- local.  *over is set if some |delta| >= b (then the exchange takes the int32 path).
+__global__ void k_wdelta_pack(const int32_t* loc, int32_t* prev, size_t n, int32_t b, uint32_t* pack, int32_t* over) {
+  bool bad = false;
+  const size_t np = (n + 1) / 2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = 2 * i;
+    const int32_t l0 = loc[e], l1 = (e + 1 < n) ? loc[e + 1] : 0;
+    const int32_t d0 = l0 - prev[e], d1 = (e + 1 < n) ? l1 - prev[e + 1] : 0;
+    bad |= (d0 >= b || d0 <= -b || d1 >= b || d1 <= -b);
+    pack[i] = (uint32_t)(d0 + b) | ((uint32_t)(d1 + b) << 16);
+    prev[e] = l0;
+    if (e + 1 < n) prev[e + 1] = l1;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31u) == 0) atomicOr(over, 1);
+}
+// out = gprev + (sum over ranks of the packed fields) - world * b
+__global__ void k_wdelta_apply(const int32_t* gprev, const uint32_t* sum, size_t n, int32_t wb, int32_t* out) {
+  const size_t np = (n + 1) / 2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < np; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = 2 * i;
+    const uint32_t v = sum[i];
+    out[e] = gprev[e] + ((int32_t)(v & 0xFFFFu) - wb);
+    if (e + 1 < n) out[e + 1] = gprev[e + 1] + ((int32_t)(v >> 16) - wb);
+  }
+}
+
 // H7 (world > 1): the W merge.  The tail tokens' topics are gathered word-major
 // (k_tail_gather); the int32 all-reduce of the dense block and the u16 all-gather of the tail
 // topics are issued as ONE NCCL group, so the two collectives run concurrently; then every
 // rank rebuilds the global packed tail rows (integer sums: W is identical on every rank).
-ezlda_status exchange_w(ezlda* h, Buf& b) {
+// The dense block goes as packed 16-bit deltas against the previous global W (gprev, the
+// other buffer) when every rank's deltas fit (one int32 all-reduce of the overflow flags
+// decides), else as the int32 local counts; gprev == nullptr forces the int32 path.
+ezlda_status exchange_w(ezlda* h, Buf& b, const Buf* gprev) {
   if (!h->multi) return EZLDA_OK;
   const bool tail = h->Vt != 0;
+  const size_t dn = (size_t)h->Vd * h->K;
+  const int32_t bias = 32768 / h->world;
+  bool delta = false;
+  if (dn && h->wpack) {  // always refresh wloc_prev; the packed deltas are usable iff it was valid
+    const bool want = gprev && h->wloc_valid && !(h->debug_flags & EZLDA_DEBUG_NO_W_DELTA);
+    EZ_CUDA(h, cudaMemsetAsync(h->wover, 0, 4, h->stream));
+    const unsigned nb = (unsigned)std::min<size_t>(((dn + 1) / 2 + 255) / 256, 148u * 16u);
+    k_wdelta_pack<<<nb, 256, 0, h->stream>>>(b.Wd, h->wloc_prev, dn, bias, h->wpack, h->wover);
+    EZ_CUDA(h, cudaGetLastError());
+    h->wloc_valid = true;
+    if (want) {
+      ezlda_status st0 = allreduce(h, h->wover, 1, ncclInt32);
+      if (st0) return st0;
+      int32_t over = 1;
+      EZ_CUDA(h, cudaMemcpyAsync(&over, h->wover, 4, cudaMemcpyDeviceToHost, h->stream));
+      EZ_CUDA(h, cudaStreamSynchronize(h->stream));
+      delta = over == 0;
+    }
+  }
+  void* dbuf = delta ? (void*)h->wpack : (void*)b.Wd;
+  const size_t dcount = delta ? (dn + 1) / 2 : dn;
+  const ncclDataType_t dtype = delta ? ncclUint32 : ncclInt32;
   if (tail && h->R > h->rt0) {
     k_tail_gather<<<(unsigned)((h->R - h->rt0 + 255) / 256), 256, 0, h->stream>>>(
         h->dev.run_j0, h->dev.run_len, h->tail_run_tok, h->rt0, h->R, b.z, h->tz_local);
     EZ_CUDA(h, cudaGetLastError());
   }
-  const size_t dense = (size_t)h->Vd * h->K, tbytes = tail ? 2ull * h->tail_max : 0;
+  const size_t tbytes = tail ? 2ull * h->tail_max : 0;
   ezlda_status st;
   if (h->lgroup) {  // in-process test hook: the same sums / concatenation, one after the other
-    if ((st = allreduce(h, b.Wd, dense, ncclInt32))) return st;
+    if ((st = allreduce(h, dbuf, dcount, dtype))) return st;
     if (tail && (st = allgather(h, h->tz_local, h->tz_all, tbytes))) return st;
   } else {
     EZ_NCCL(h, nccl().GroupStart());
-    if (dense) EZ_NCCL(h, nccl().AllReduce(b.Wd, b.Wd, dense, ncclInt32, ncclSum, h->comm, h->stream));
+    if (dcount) EZ_NCCL(h, nccl().AllReduce(dbuf, dbuf, dcount, dtype, ncclSum, h->comm, h->stream));
     if (tbytes) EZ_NCCL(h, nccl().AllGather(h->tz_local, h->tz_all, tbytes, ncclUint8, h->comm, h->stream));
     EZ_NCCL(h, nccl().GroupEnd());
   }
+  if (delta) {
+    const unsigned nb = (unsigned)std::min<size_t>(((dn + 1) / 2 + 255) / 256, 148u * 16u);
+    k_wdelta_apply<<<nb, 256, 0, h->stream>>>(gprev->Wd, h->wpack, dn, bias * h->world, b.Wd);
+    EZ_CUDA(h, cudaGetLastError());
+    ++h->delta_exchanges;
+  }
+  h->exchange_bytes = 4.0 * (double)dcount + (double)h->world * (double)tbytes;
   if (tail) {
     ezl::launch_tail_rebuild(h->dev, b, h->tz_all, h->tail_off, (uint32_t)h->world, h->tail_max, h->stream);
     EZ_CUDA(h, cudaGetLastError());
@@ -624,7 +696,7 @@ ezlda_status rebuild_counts(ezlda* h) {
   ezl::launch_sampler(h->dev, b, b, h->n_items, 0, true, h->stream);
   EZ_CUDA(h, cudaGetLastError());
   ezlda_status s;
-  if ((s = exchange_w(h, b))) return s;
+  if ((s = exchange_w(h, b, nullptr))) return s;  // int32 path (no previous exchange to delta against)
   ezl::launch_nk(h->dev, b, h->stream);  // n_k of the global W (identical on every rank)
   EZ_CUDA(h, cudaGetLastError());
   h->D_fresh = false;
@@ -927,6 +999,12 @@ ezlda_status do_create(ezlda* h, const uint32_t* word_ids, const uint32_t* doc_i
     EZ_CUDA(h, cudaStreamSynchronize(s));
   }
   if (h->multi) h->exchange_bytes = 4.0 * (double)h->Vd * h->K + 2.0 * h->world * (h->Vt ? h->tail_max : 0);
+  if (h->multi && (size_t)h->Vd * h->K) {
+    const size_t dn = (size_t)h->Vd * h->K;
+    EZ_ALLOC(h, h->wloc_prev, int32_t, dn);
+    EZ_ALLOC(h, h->wpack, uint32_t, (dn + 1) / 2);
+    EZ_ALLOC(h, h->wover, int32_t, 1);
+  }
   h->release(tokpre);
   h->release(wrun);
   // order: hot-word items window-major, heavy first within a window; then the other items
@@ -1359,7 +1437,7 @@ ezlda_status ezlda_iterate(ezlda* h, uint32_t n_iters) {
     ezlda_status st;
     // H7 (world > 1): all-reduce of the dense block + all-gather of the tail
     // topics (one NCCL group) + tail-row rebuild; n_k from the merged W
-    if ((st = exchange_w(h, nxt))) return st;
+    if ((st = exchange_w(h, nxt, &cur))) return st;
     if (h->multi) ezl::launch_nk(h->dev, nxt, s);  // n_k of the global W (identical on every rank)
     EZ_CUDA(h, cudaGetLastError());
     EZ_CUDA(h, cudaMemcpyAsync(h->ctr_host + si, h->dev.ctr, sizeof(ezl::Counters), cudaMemcpyDeviceToHost, s));

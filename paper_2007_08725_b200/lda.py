@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("EZLDA_LIB") or os.path.join(HERE, "libezlda.so")
 
 EZLDA_W_HYBRID, EZLDA_W_ALL_DENSE, EZLDA_W_ALL_SPARSE = 0, 1, 2
 EZLDA_DEBUG_NO_TAIL_ROWS, EZLDA_DEBUG_C1_LOOKUP, EZLDA_DEBUG_DPERM_ON, EZLDA_DEBUG_DPERM_OFF = 1, 2, 4, 8
+EZLDA_DEBUG_NO_W_DELTA = 16
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_RANGE", 3: "E_NOMEM", 4: "E_CUDA", 5: "E_NCCL", 6: "E_STATE"}
 
 # every symbol include/ezlda.h declares

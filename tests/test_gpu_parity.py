@@ -316,12 +316,15 @@ def test_invalid_arguments(ez):
 
 @pytest.mark.parametrize("sampler", [3, 2])
 @pytest.mark.parametrize("world", [2, 3])
-def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler):
+@pytest.mark.parametrize("delta", [True, False])
+def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler, delta):
     """The library's multi-rank path (doc shards with token bases, global word counts and
-    relabelling, all-dense W merged every iteration, LLPT reduction) with the ranks as
-    handles of this process on one GPU (options.local_group: the merge is an in-process
-    device sum instead of NCCL).  Concatenated topics, W, n_k and LLPT must equal the
-    single-rank chain bit for bit (P-invariance of the counter-based draws)."""
+    relabelling, the hybrid W merged every iteration -- the dense block as packed 16-bit deltas
+    against the previous W (default) or as int32 counts (EZLDA_DEBUG_NO_W_DELTA), the tail as
+    all-gathered topics -- LLPT reduction) with the ranks as handles of this process on one
+    GPU (options.local_group: the merge is an in-process device sum instead of NCCL).
+    Concatenated topics, W, n_k and LLPT must equal the single-rank chain bit for bit
+    (P-invariance of the counter-based draws), and the exchanged bytes the path's size."""
     import threading
 
     w, d = planted_corpus_np(n_docs=600, V=4000, mean_len=90.0, sigma=0.5, seed=17)
@@ -339,9 +342,11 @@ def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler):
         try:
             t0, t1 = int(cum[b[r]]), int(cum[b[r + 1]])
             h = ez.EzLDA(w[t0:t1], d[t0:t1] - b[r], b[r + 1] - b[r], V, K, seed=SAMPLER_SEED, rank=r, world=world,
-                         token_base=t0, local_group=1000 + 10 * sampler + world, sampler=sampler)
+                         token_base=t0, local_group=1000 + 100 * int(delta) + 10 * sampler + world, sampler=sampler,
+                         debug_flags=0 if delta else ez.EZLDA_DEBUG_NO_W_DELTA)
             h.iterate(iters)
-            out[r] = (h.topics(), ez.EzLDA.csr_to_dense(*h.W_csr(), K), h.n_k(), h.loglik())
+            xb = h.stats()["exchange_bytes"]
+            out[r] = (h.topics(), ez.EzLDA.csr_to_dense(*h.W_csr(), K), h.n_k(), h.loglik(), xb)
         except Exception as e:  # surfaced below (the other ranks would wait forever otherwise)
             errs.append(repr(e))
 
@@ -363,6 +368,15 @@ def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler):
         assert np.array_equal(out[r][1], W_ref), r
         assert np.array_equal(out[r][2], nk_ref), r
         assert abs(out[r][3] - ll_ref) <= 1e-12 * abs(ll_ref), (out[r][3], ll_ref)
+    # bytes of the last exchange: dense block (Vd x K: packed u32 pairs, or int32) + the tail
+    # all-gather (world slots of the largest local tail-token count, u16)
+    cnt = np.bincount(w, minlength=V)
+    dense_words = cnt > K
+    Vd = int(dense_words.sum())
+    tail_max = max(int((~dense_words[w[int(cum[b[r]]):int(cum[b[r + 1]])]]).sum()) for r in range(world))
+    dense_bytes = 4 * ((Vd * K + 1) // 2) if delta else 4 * Vd * K
+    for r in range(world):
+        assert out[r][4] == dense_bytes + world * 2 * tail_max, (r, out[r][4], dense_bytes, tail_max)
 
 
 TWO_BRANCH_CASES = {
