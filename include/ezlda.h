@@ -155,9 +155,10 @@ typedef struct {
   uint64_t kernel_launches;  /* library kernels launched by the iteration                  */
   uint64_t exact_redraws;    /* sampled tokens redrawn on the exact fp64 path (fixed-point decision
                                 not certified by its error margin)      */
-  double exchange_bytes;     /* H7 collective payload of the iteration (world > 1): int32 all-  */
-                             /* reduce of the dense W block + n_k, u16 all-gather of the tail  */
-                             /* topics (output size); 0 when world == 1                        */
+  double exchange_bytes;     /* H7 collective payload of the iteration (world > 1): all-reduce  */
+                             /* of the dense W block (packed 16-bit deltas: 2 B per entry, or  */
+                             /* int32 counts: 4 B) + u16 all-gather of the tail topics (output */
+                             /* size); 0 when world == 1                                       */
   double ms_sampler_kernel;  /* the k_sampler launch alone (inside ms_sample, which also holds  */
                              /* the H4 item schedule and the n_k column sums)                   */
 } ezlda_iter_stats;

@@ -488,8 +488,9 @@ ezlda_status local_allreduce(ezlda* h, void* buf, size_t count, ncclDataType_t d
   }
   if (!group_barrier(g)) return h->fail(EZLDA_E_STATE, "local group barrier timed out (a rank failed)");
   void* tmp = nullptr;
-  EZ_CUDA(h, cudaMalloc(&tmp, count * esz + sizeof(void*) * g->world));
-  const void** d_src = reinterpret_cast<const void**>(static_cast<char*>(tmp) + count * esz);
+  const size_t src_off = (count * esz + 15) & ~(size_t)15;  // the pointer table 16-byte aligned
+  EZ_CUDA(h, cudaMalloc(&tmp, src_off + sizeof(void*) * g->world));
+  const void** d_src = reinterpret_cast<const void**>(static_cast<char*>(tmp) + src_off);
   EZ_CUDA(h, cudaMemcpyAsync(d_src, g->bufs.data(), sizeof(void*) * g->world, cudaMemcpyHostToDevice, h->stream));
   const unsigned nb = (unsigned)std::min<size_t>((count + 255) / 256, 4096);
   if (dt == ncclInt32)
