@@ -86,7 +86,25 @@ def test_two_rank_gloo_equals_single(tmp_path, branches):
     assert np.array_equal(np.load(out), ref.topics().astype(np.int64))
 
 
-def worker_hybrid(rank, world, port, out):
+def pack_delta(delta, b):
+    """The library's k_wdelta_pack on the host: int deltas -> u32 pairs (delta + b) | (delta' + b) << 16
+    (as int64 tensors: gloo has no u32 sum; every sum stays below 2^32)."""
+    flat = delta.ravel().astype(np.int64)
+    if len(flat) % 2:
+        flat = np.concatenate([flat, [0]])
+    return torch.from_numpy((flat[0::2] + b) | ((flat[1::2] + b) << 16))
+
+
+def unpack_sum(psum, n, world, b):
+    """k_wdelta_apply's decoding: the per-field sums minus world * b, first n entries."""
+    v = psum.numpy()
+    out = np.empty(2 * len(v), np.int64)
+    out[0::2] = (v & 0xFFFF) - world * b
+    out[1::2] = (v >> 16) - world * b
+    return out[:n]
+
+
+def worker_hybrid(rank, world, port, out, delta=False):
     """The library's H7 protocol on CPU: global word counts decide the dense set
     (c_v > K); per iteration the dense block [V_d x K] and n_k are all-reduced (sum), and the
     tail words' topics are all-gathered in word-major order (padded to the largest rank's
@@ -115,12 +133,33 @@ def worker_hybrid(rank, world, port, out):
     sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(sizes, n_loc)
     tail_max = int(max(s.item() for s in sizes))
+    b = 32768 // world
+    loc_prev = glob_prev = None
+    n_delta = 0
     for _ in range(ITERS):
         z = shard.topics()
         Wl = shard.counts()[1].astype(np.int64)
         Wd = torch.from_numpy(Wl[dense].copy())
         nk = torch.from_numpy(Wl.sum(0))
-        dist.all_reduce(Wd)
+        if delta and loc_prev is not None:
+            # packed 16-bit deltas against the previous exchange (exchange_w): one flag
+            # all-reduce decides, then the u32-pair sum rebuilds the global block
+            dl = Wl[dense] - loc_prev
+            over = torch.tensor([int(np.any(np.abs(dl) >= b))])
+            dist.all_reduce(over)
+            full = Wd.clone()
+            dist.all_reduce(full)  # (check only: the int32 path's result)
+            if int(over.item()) == 0:
+                ps = pack_delta(dl, b)
+                dist.all_reduce(ps)
+                rebuilt = glob_prev + unpack_sum(ps, dl.size, world, b).reshape(dl.shape)
+                assert np.array_equal(rebuilt, full.numpy())
+                n_delta += 1
+            Wd = full
+        else:
+            dist.all_reduce(Wd)
+        loc_prev = Wl[dense].copy()
+        glob_prev = Wd.numpy().copy()
         dist.all_reduce(nk)
         tz = torch.full((tail_max, 2), -1, dtype=torch.int64)  # (word, topic) of each tail token
         tz[: len(local_tail_tok), 0] = torch.from_numpy(ws[local_tail_tok].astype(np.int64))
@@ -141,19 +180,23 @@ def worker_hybrid(rank, world, port, out):
     pad[: len(zt)] = zt
     allp = [torch.zeros(mx, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(allp, pad)
+    if delta:
+        assert n_delta >= 1, "the delta path was never taken"
     if rank == 0:
         np.save(out, np.concatenate([p[p >= 0].numpy() for p in allp]))
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_hybrid_exchange_equals_single(tmp_path):
-    """Dense-block all-reduce + tail-topic all-gather (the H7 protocol of the library) equals
-    the single chain bit for bit."""
+@pytest.mark.parametrize("delta", [False, True])
+def test_two_rank_gloo_hybrid_exchange_equals_single(tmp_path, delta):
+    """Dense-block all-reduce (int32 counts, or packed 16-bit deltas against the previous
+    exchange whose decoded sum must equal the int32 one) + tail-topic all-gather (the H7
+    protocol of the library) equals the single chain bit for bit."""
     from oracle import oracle
 
     oracle.build()
     out = str(tmp_path / "z.npy")
-    mp.spawn(worker_hybrid, args=(2, free_port(), out), nprocs=2, join=True)
+    mp.spawn(worker_hybrid, args=(2, free_port(), out, delta), nprocs=2, join=True)
     w, d = planted_corpus_np(N_DOCS, V, 80.0, 0.5, seed=11)
     ref = oracle.OracleLDA(w, d, N_DOCS, V, K, seed=SAMPLER_SEED)
     ref.iterate(ITERS)
