@@ -11,7 +11,9 @@
 //     8-word header and are zero padded to a multiple of 8 entries, so the sampler reads
 //     whole sectors without masking):
 //     D[ddb] = (L_d << 16) | nnz_d, D[ddb+1] = dofs[d], D[ddb+8+i] = (topic << 18) | count
-//     sorted by topic (packed CSR; rebuilt every iteration)
+//     sorted by topic (packed CSR; rebuilt every iteration); long-doc
+//     shards with K <= 4096 (Dev::dperm): entries 128-byte aligned (ddb = 24 mod 32 words),
+//     capacity 32 + roundup64(min(L_d, K)), logical entry i at D[ddb+8+d_phys(i)] (below)
 //   word-major runs r in [0, R) (runs of word v contiguous, docs ascending):
 //     run_j0[r] u32 first doc-major token, run_dbase[r] u32 D-row base, run_len[r] u16
 //   flags[R/32] u32: run r holds a token that failed the MPT skip test (L2 resident)
@@ -19,8 +21,9 @@
 //     min(c_v, K) at tofs[v-Vd]) with tnnz[v-Vd]; double-buffered with n_k[K].
 //   rec[V] WordRec (48 B): top-4 topics/values and Q' of every word.
 //   wrow[Vw][rs_bytes]: sampler heads of the words with a live item: u32 m[Kpad] (fixed-point
-//     What', K1 entry 0) | f64 {2^-s, 2^s, 2^-t, 2^t} | u32 qfx[Kpad] (fixed-point Q' prefix)
-//     | u32 ce[] (its chunk ends); bulk-copied (TMA) into a sampler slot.  Words v >= Vw (when
+//     What', K1 entry 0) | f64 {2^-s, 2^s, 2^-t, 2^t} | u32 qfx[Kpad] (fixed-point Q' prefix,
+//     XOR-swizzled within 32-topic chunks: q_swz) | u32 ce[] (its chunk ends); bulk-copied (TMA)
+//     into a sampler slot.  Words v >= Vw (when
 //     V heads do not fit in HBM) are staged by a sampler warp (stage_row_warp).
 //   items: (word, run range, tokens): the sampler's work list, heavy first.
 #pragma once
