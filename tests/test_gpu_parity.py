@@ -317,7 +317,7 @@ def test_invalid_arguments(ez):
 @pytest.mark.parametrize("sampler", [3, 2])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("delta", [True, False])
-def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler, delta):
+def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler, delta, dperm=False):
     """The library's multi-rank path (doc shards with token bases, global word counts and
     relabelling, the hybrid W merged every iteration -- the dense block as packed 16-bit deltas
     against the previous W (default) or as int32 counts (EZLDA_DEBUG_NO_W_DELTA), the tail as
@@ -342,8 +342,9 @@ def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler, delta):
         try:
             t0, t1 = int(cum[b[r]]), int(cum[b[r + 1]])
             h = ez.EzLDA(w[t0:t1], d[t0:t1] - b[r], b[r + 1] - b[r], V, K, seed=SAMPLER_SEED, rank=r, world=world,
-                         token_base=t0, local_group=1000 + 100 * int(delta) + 10 * sampler + world, sampler=sampler,
-                         debug_flags=0 if delta else ez.EZLDA_DEBUG_NO_W_DELTA)
+                         token_base=t0, local_group=1000 + 200 * int(dperm) + 100 * int(delta) + 10 * sampler + world,
+                         sampler=sampler, debug_flags=(0 if delta else ez.EZLDA_DEBUG_NO_W_DELTA)
+                         | (ez.EZLDA_DEBUG_DPERM_ON if dperm else 0))
             h.iterate(iters)
             xb = h.stats()["exchange_bytes"]
             out[r] = (h.topics(), ez.EzLDA.csr_to_dense(*h.W_csr(), K), h.n_k(), h.loglik(), xb)
@@ -377,6 +378,12 @@ def test_multi_rank_library_path_one_gpu(ez, oracle_mod, world, sampler, delta):
     dense_bytes = 4 * ((Vd * K + 1) // 2) if delta else 4 * Vd * K
     for r in range(world):
         assert out[r][4] == dense_bytes + world * 2 * tail_max, (r, out[r][4], dense_bytes, tail_max)
+
+
+@pytest.mark.parametrize("sampler", [3, 2])
+def test_multi_rank_interleaved_rows(ez, oracle_mod, sampler):
+    """The multi-rank path with every rank's D rows sector-interleaved (forced on short docs)."""
+    test_multi_rank_library_path_one_gpu(ez, oracle_mod, 2, sampler, True, dperm=True)
 
 
 TWO_BRANCH_CASES = {
