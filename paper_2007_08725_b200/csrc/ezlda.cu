@@ -100,6 +100,9 @@ __global__ void k_max_u16(const uint16_t* a, uint64_t n, uint32_t* out) {
 #ifndef EZLDA_DPERM_MIN_MEAN_L
 #define EZLDA_DPERM_MIN_MEAN_L 192
 #endif
+#ifndef EZLDA_POOL
+#define EZLDA_POOL 0  // A/B (profiles/r02/ab_dperm.log): create time and e2e within the run-to-run noise either way
+#endif
 static uint32_t dperm_of(uint32_t K, uint64_t N, uint32_t Dn, uint32_t flags) {
   if (!ezl::kDPermOn || K > ezl::kDPermMaxK || (flags & EZLDA_DEBUG_DPERM_OFF)) return 0u;
   if (flags & EZLDA_DEBUG_DPERM_ON) return 1u;
@@ -356,17 +359,27 @@ struct ezlda {
     return s;
   }
 
+  // Optional (EZLDA_POOL build switch, off): device memory from a private stream-ordered pool,
+  // so that create's many GB of transients are reused instead of mapped and unmapped by
+  // cudaMalloc / cudaFree; trimmed when create ends, destroyed with the handle.  Measured within
+  // the (large) run-to-run noise of create, so the default stays cudaMalloc.
+  cudaMemPool_t pool = nullptr;
   template <typename T>
   T* alloc(size_t n) {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) return nullptr;
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    if (pool) {
+      if (cudaMallocFromPoolAsync(&p, bytes, pool, stream) != cudaSuccess) return nullptr;
+    } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      return nullptr;
+    }
     allocs.push_back(p);
     return static_cast<T*>(p);
   }
   void release(void* p) {
     auto it = std::find(allocs.begin(), allocs.end(), p);
     if (it != allocs.end()) {
-      cudaFree(p);
+      if (pool) cudaFreeAsync(p, stream); else cudaFree(p);
       allocs.erase(it);
     }
   }
@@ -398,10 +411,10 @@ template <typename F>
 ezlda_status cub_call(ezlda* h, F f) {
   size_t bytes = 0;
   if (f(nullptr, bytes) != cudaSuccess) return h->fail(EZLDA_E_CUDA, "cub size query failed");
-  void* tmp = nullptr;
-  if (cudaMalloc(&tmp, std::max<size_t>(bytes, 1)) != cudaSuccess) return h->fail(EZLDA_E_NOMEM, "cub temp alloc");
+  void* tmp = h->alloc<unsigned char>(bytes);
+  if (!tmp) return h->fail(EZLDA_E_NOMEM, "cub temp alloc");
   cudaError_t e = f(tmp, bytes);
-  cudaFree(tmp);
+  h->release(tmp);
   if (e != cudaSuccess) return h->fail(EZLDA_E_CUDA, "cub call failed: %s", cudaGetErrorString(e));
   return EZLDA_OK;
 }
@@ -1350,6 +1363,22 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
     }
     h->own_stream = true;
   }
+#if EZLDA_POOL
+  {
+    int dev = 0;
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    if (cudaGetDevice(&dev) == cudaSuccess) pp.location.id = dev;
+    if (cudaMemPoolCreate(&h->pool, &pp) == cudaSuccess) {
+      uint64_t keep = ~0ull;  // freed blocks stay in the pool (reused by later allocations of create)
+      cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    } else {
+      h->pool = nullptr;
+      cudaGetLastError();
+    }
+  }
+#endif
   if (h->multi && o.local_group) {
     if (o.rank < 0 || o.rank >= h->world) st = h->fail(EZLDA_E_INVALID, "local_group needs 0 <= rank < world");
     else if (!(h->lgroup = local_group_join(o.local_group, h->world)))
@@ -1369,6 +1398,10 @@ ezlda_status ezlda_create(const uint32_t* word_ids, const uint32_t* doc_ids, uin
     }
   }
   if (!st) st = do_create(h, word_ids, doc_ids, o);
+  if (!st && h->pool) {  // give the transients' memory back (the steady state keeps its own buffers)
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess) st = h->fail(EZLDA_E_CUDA, "create: stream sync failed");
+    else cudaMemPoolTrimTo(h->pool, 0);
+  }
   if (st) {
     g_create_error = h->err;
     ezlda_destroy(h);
@@ -1630,8 +1663,15 @@ const char* ezlda_last_error(const ezlda* h) { return h ? h->err.c_str() : g_cre
 void ezlda_destroy(ezlda* h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
-  for (void* p : h->allocs) cudaFree(p);
+  for (void* p : h->allocs) {
+    if (h->pool) cudaFreeAsync(p, h->stream); else cudaFree(p);
+  }
   h->allocs.clear();
+  if (h->pool) {
+    cudaStreamSynchronize(h->stream);
+    cudaMemPoolDestroy(h->pool);
+    h->pool = nullptr;
+  }
   if (h->ctr_host) cudaFreeHost(h->ctr_host);
   for (auto& sl : h->slots)
     for (auto& e : sl.ev)
