@@ -488,11 +488,13 @@ __device__ __forceinline__ uint32_t row_lookup(const uint16_t* keys, const uint1
 // the sampler's marker) and returns true if the token failed the test (its run must be flagged).
 template <typename LookupF>
 __device__ __forceinline__ bool mpt_token(const Dev& d, const Buf& nxt, uint32_t j, uint32_t L, uint32_t iter,
-                                          uint32_t v, LookupF C, unsigned long long& n_skip, bool g2) {
+                                          uint32_t v, LookupF C, unsigned long long& n_skip, bool g2,
+                                          uint32_t kk_pre = 0xFFFFFFFFu) {
   WordRec r;
   if (g2) {  // g <= 2 (a warp-uniform kernel argument): compact view, one 32-byte load + one 4-byte load
     const WordRecM m = d.recm[v];
-    const uint32_t kk = __ldg(d.reck + v);
+    // K1 | K2 << 16, loaded ahead by the caller when it can (the counter lookups wait on it)
+    const uint32_t kk = (kk_pre != 0xFFFFFFFFu) ? kk_pre : __ldg(d.reck + v);
     r.a[0] = m.a0;
     r.a[1] = m.a1;
     r.a[2] = m.a2;
@@ -575,6 +577,9 @@ template <bool kSkipTest, bool kG2 = true>  // kG2: S_est depth g <= 2 (the comp
 #ifndef EZLDA_DOC_PF
 #define EZLDA_DOC_PF 1
 #endif
+#ifndef EZLDA_DOC_KKPF
+#define EZLDA_DOC_KKPF 0  // A/B: 10.22 -> 10.38 ms at PubMed (profiles/r02/ab_dperm.log), off
+#endif
 #ifndef EZLDA_DOC_MINB
 #define EZLDA_DOC_MINB 4
 #endif
@@ -629,6 +634,14 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       pv[c] = wr.x;
       pr[c] = wr.y;
     }
+#if EZLDA_DOC_KKPF
+    // the first rounds' K1 | K2 words requested before the histogram is built, so that their
+    // latency overlaps the shared-memory atomics instead of stalling the counter lookups
+    uint32_t pkk[kPre];
+#pragma unroll
+    for (uint32_t c = 0; c < kPre; ++c)
+      pkk[c] = (kSkipTest && kG2 && lane + 32u * c < L) ? __ldg(d.reck + pv[c]) : 0xFFFFFFFFu;
+#endif
 #pragma unroll
     for (uint32_t c = 0; c < kPre; ++c) {
       if (lane + 32u * c < L) {
@@ -649,7 +662,11 @@ __global__ void __launch_bounds__(kDocWarps * 32, EZLDA_DOC_MINB) k_doc_hist(Dev
       for (uint32_t c = 0; c < kPre; ++c) {
         if (32u * c >= L) break;  // warp-uniform
         bool f = false;
+#if EZLDA_DOC_KKPF
+        if (lane + 32u * c < L) f = mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], C, n_skip, kG2, pkk[c]);
+#else
         if (lane + 32u * c < L) f = mpt_token(d, nxt, j0 + lane + 32u * c, L, iter, pv[c], C, n_skip, kG2);
+#endif
 #ifndef EZLDA_EXP_DOC_NOFLAG  // diagnostic: no flag atomics (the sampler then sees no flagged run)
         flag_run(d, f, pr[c]);
 #endif
