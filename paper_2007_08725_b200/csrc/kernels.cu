@@ -881,6 +881,9 @@ __device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over
 // i ^ (chunk & 31)): the lanes of a warp search different chunks in step, so an unswizzled
 // table sends them all to the same bank (e.g. every lane's first probe is entry 15 of its chunk)
 __device__ __forceinline__ uint32_t q_swz(uint32_t i) { return EZLDA_QSWZ ? (i ^ ((i >> 5) & 31u)) : i; }
+#ifndef EZLDA_QG_VEC
+#define EZLDA_QG_VEC 0  // A/B at K = 10k: 42.91 -> 43.02 ms (profiles/r02/ab_dperm.log), off
+#endif
 #ifndef EZLDA_LARGEK_1BLK
 #define EZLDA_LARGEK_1BLK 0  // A/B: 1 block x 3-4 slots at K = 10k 42.5 -> 57-59 ms (profiles/r02/ab_dperm.log)
 #endif
@@ -1519,9 +1522,26 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
             a = 32u * ca;
             b = a + 31u;
           }
-          while (a < b) {
-            const uint32_t mid = (a + b) >> 1;
-            if (qv(mid) > Yq) b = mid; else a = mid + 1u;
+          if (kQG && EZLDA_QG_VEC) {
+            // HBM table (large K): the chunk's 32 entries (one 128-byte line) with 8 independent
+            // 16-byte loads instead of 5 dependent probes; qfx is non-decreasing, so the first
+            // entry > Yq sits at the count of entries <= Yq (the swizzle only permutes the line)
+            const uint4* q4 = reinterpret_cast<const uint4*>(qfx + a);
+            uint32_t cnt = 0;
+#pragma unroll 1
+            for (int h2 = 0; h2 < 8; h2 += 4) {  // two groups of four loads (register budget)
+              uint4 x[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) x[q] = __ldca(q4 + h2 + q);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) cnt += (x[q].x <= Yq) + (x[q].y <= Yq) + (x[q].z <= Yq) + (x[q].w <= Yq);
+            }
+            a += min(cnt, 31u);
+          } else {
+            while (a < b) {
+              const uint32_t mid = (a + b) >> 1;
+              if (qv(mid) > Yq) b = mid; else a = mid + 1u;
+            }
           }
           // + one qfx ulp + the bound (K + 4) 2^-52 Q' on the difference between the staged
           // chunked prefix and the oracle's sequential one (stage_row_warp)
