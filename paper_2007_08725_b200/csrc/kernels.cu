@@ -881,6 +881,9 @@ __device__ uint32_t g_fake[1024 + 16];  // (topic << 18) | 1, topics spread over
 // i ^ (chunk & 31)): the lanes of a warp search different chunks in step, so an unswizzled
 // table sends them all to the same bank (e.g. every lane's first probe is entry 15 of its chunk)
 __device__ __forceinline__ uint32_t q_swz(uint32_t i) { return EZLDA_QSWZ ? (i ^ ((i >> 5) & 31u)) : i; }
+#ifndef EZLDA_ZPRE2
+#define EZLDA_ZPRE2 0  // A/B: 72.7-73.0 -> 73.4-73.6 ms at PubMed (spills), off
+#endif
 #ifndef EZLDA_QG_VEC
 #define EZLDA_QG_VEC 0  // A/B at K = 10k: 42.91 -> 43.02 ms (profiles/r02/ab_dperm.log), off
 #endif
@@ -1262,6 +1265,15 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     const uint32_t j = __shfl_sync(kFull, j0, slot) + (lane - __shfl_sync(kFull, tofs, slot));
     if (lane < ntb) zpre = nxt.z[j];
   }
+#if EZLDA_ZPRE2
+  // ... and those of the second round (a batch of ~32 short runs holds 33-64 tokens)
+  uint32_t zpre2 = 0;
+  if (ntb > 32u) {
+    const uint32_t slot = slot_of(32u, tofs);
+    const uint32_t j = __shfl_sync(kFull, j0, slot) + (32u + lane - __shfl_sync(kFull, tofs, slot));
+    if (32u + lane < ntb) zpre2 = nxt.z[j];
+  }
+#endif
   // ---- B: lane per segment (kSegW entries = kSegW / 8 sectors); consecutive lanes read
   //      consecutive sectors of a row.  Exact integer sums of D[d][k] m_v[k] (m_v the word's
   //      fixed-point What' row), combined by a segmented warp scan (+ carry across rounds).
@@ -1391,7 +1403,11 @@ __device__ __forceinline__ uint32_t sample_batch(const Dev& d, const Buf& cur, c
     if (i >= ntb) continue;
     const uint32_t j = s_j0 + (i - s_tofs);
     const uint32_t* E = d.D + s_ebase;
+#if EZLDA_ZPRE2
+    const uint32_t zm = B0 == 0u ? zpre : B0 == 32u ? zpre2 : (uint32_t)nxt.z[j];
+#else
     const uint32_t zm = B0 ? (uint32_t)nxt.z[j] : zpre;
+#endif
     uint32_t C1;
     if (d.zmark) {
       if (!(zm & 0x8000u)) continue;  // skipped by the MPT test (z^i = K1 < 0x8000)
